@@ -1,0 +1,625 @@
+// engine.cpp -- device-resident renderer: scene upload (Morton-ordered SoA in
+// HBM), per-frame tile binning, the render launch with its wide-window retry
+// pass, statistics, and the NCCL tile gather for image-tile sharding over
+// ranks.
+#include "engine.hpp"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+
+namespace sphray_b200 {
+
+#define CUDA_OK(x)                                                                 \
+    do {                                                                           \
+        cudaError_t e_ = (x);                                                      \
+        if (e_ != cudaSuccess)                                                     \
+            fail(SPHRAY_ERR_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+void DevBuf::ensure(size_t b) {
+    if (b <= bytes && p) return;
+    release();
+    const size_t want = std::max<size_t>(b, 256);
+    CUDA_OK(cudaMalloc(&p, want));
+    bytes = want;
+}
+
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+
+void HostPinned::ensure(size_t b) {
+    if (b <= bytes && p) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    CUDA_OK(cudaMallocHost(&p, b));
+    bytes = b;
+}
+
+HostPinned::~HostPinned() {
+    if (p) cudaFreeHost(p);
+}
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded at runtime so single-GPU use has no NCCL dependency and the
+// process shares whichever libnccl.so.2 (e.g. torch's) is already resident.
+namespace {
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.why = std::string("cannot load libnccl: ") + dlerror();
+            return a;
+        }
+        a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+        a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+        a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+        a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.GetUniqueId && a.CommInitRank && a.AllGather && a.CommDestroy && a.GetErrorString;
+        if (!a.ok) a.why = "libnccl is missing symbols";
+        return a;
+    }();
+    return api;
+}
+
+void nccl_ok(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        fail(SPHRAY_ERR_NCCL, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+}  // namespace
+
+void comm_unique_id(uint8_t out[128]) {
+    auto& a = nccl();
+    if (!a.ok) fail(SPHRAY_ERR_NCCL, a.why);
+    ncclUniqueId id;
+    nccl_ok(a.GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+}
+
+// ---------------------------------------------------------------------------
+Engine::Engine(int device) : device_(device) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        fail(SPHRAY_ERR_CUDA, "no CUDA device available (the GPU path has no CPU fallback)");
+    if (device < 0 || device >= count) fail(SPHRAY_ERR_CUDA, "device index out of range");
+    set_device();
+    cudaDeviceProp prop{};
+    CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        fail(SPHRAY_ERR_CUDA, std::string("device ") + prop.name + " is not sm_100 (B200) class");
+    sm_count_ = prop.multiProcessorCount;
+    CUDA_OK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreate(&ev0_));
+    CUDA_OK(cudaEventCreate(&ev1_));
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    if (comm_ && nccl().ok) nccl().CommDestroy(static_cast<ncclComm_t>(comm_));
+    if (ev0_) cudaEventDestroy(ev0_);
+    if (ev1_) cudaEventDestroy(ev1_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::set_device() const { CUDA_OK(cudaSetDevice(device_)); }
+
+void Engine::init_comm(int rank, int nranks, const uint8_t id[128]) {
+    set_device();
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(SPHRAY_ERR_CONFIG, "bad rank / nranks");
+    if (nranks == 1) {
+        rank_ = 0;
+        nranks_ = 1;
+        return;
+    }
+    auto& a = nccl();
+    if (!a.ok) fail(SPHRAY_ERR_NCCL, a.why);
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    ncclComm_t c = nullptr;
+    nccl_ok(a.CommInitRank(&c, nranks, uid, rank), "ncclCommInitRank");
+    if (comm_) a.CommDestroy(static_cast<ncclComm_t>(comm_));
+    comm_ = c;
+    rank_ = rank;
+    nranks_ = nranks;
+}
+
+void Engine::set_shard(int rank, int nranks) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(SPHRAY_ERR_CONFIG, "bad rank / nranks");
+    if (comm_ && nccl().ok) nccl().CommDestroy(static_cast<ncclComm_t>(comm_));
+    comm_ = nullptr;
+    rank_ = rank;
+    nranks_ = nranks;
+}
+
+void Engine::upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_view& lutv) {
+    set_device();
+    lut_ = make_lut(lutv);
+    if (n >= static_cast<size_t>(INT32_MAX)) fail(SPHRAY_ERR_CONFIG, "too many particles");
+    if (n > 0 && !ps) fail(SPHRAY_ERR_CONFIG, "null particle pointer");
+    n_ = n;
+    const int D = lut_.D;
+    d_lut_.ensure(lut_.rows.size() * sizeof(double));
+    CUDA_OK(cudaMemcpyAsync(d_lut_.p, lut_.rows.data(), lut_.rows.size() * sizeof(double),
+                            cudaMemcpyHostToDevice, stream_));
+    has_scene_ = true;
+    if (n == 0) {
+        CUDA_OK(cudaStreamSynchronize(stream_));
+        return;
+    }
+    // pow(h, d+3) with glibc (quantize.hpp:222): the one libm call per particle
+    h_powh_.resize(n * D);
+    particle_powers(ps, n, D, h_powh_.data());
+    double lo[3] = {ps[0].x, ps[0].y, ps[0].z}, hi[3] = {ps[0].x, ps[0].y, ps[0].z};
+    for (size_t i = 1; i < n; ++i) {
+        lo[0] = std::min(lo[0], ps[i].x);
+        lo[1] = std::min(lo[1], ps[i].y);
+        lo[2] = std::min(lo[2], ps[i].z);
+        hi[0] = std::max(hi[0], ps[i].x);
+        hi[1] = std::max(hi[1], ps[i].y);
+        hi[2] = std::max(hi[2], ps[i].z);
+    }
+    double inv[3];
+    for (int a = 0; a < 3; ++a) {
+        const double ext = hi[a] - lo[a];
+        inv[a] = (ext > 0.0 && std::isfinite(ext)) ? 2097151.0 / ext : 0.0;
+        if (!std::isfinite(lo[a])) lo[a] = 0.0;
+    }
+    d_raw_.ensure(n * sizeof(sphray_particle));
+    d_powh_raw_.ensure(n * D * sizeof(double));
+    CUDA_OK(cudaMemcpyAsync(d_raw_.p, ps, n * sizeof(sphray_particle), cudaMemcpyHostToDevice, stream_));
+    CUDA_OK(cudaMemcpyAsync(d_powh_raw_.p, h_powh_.data(), n * D * sizeof(double),
+                            cudaMemcpyHostToDevice, stream_));
+    d_codes_.ensure(n * 8);
+    d_codes2_.ensure(n * 8);
+    d_idx_.ensure(n * 4);
+    d_idx2_.ensure(n * 4);
+    launch_morton(d_raw_.as<sphray_particle>(), n, lo, inv, d_codes_.as<unsigned long long>(),
+                  d_idx_.as<uint32_t>(), stream_);
+    const size_t sb = cub_sort_bytes(n, 63);
+    d_tmp_.ensure(sb);
+    cub_sort(d_codes_.as<unsigned long long>(), d_codes2_.as<unsigned long long>(),
+             d_idx_.as<uint32_t>(), d_idx2_.as<uint32_t>(), n, 63, d_tmp_.p, d_tmp_.bytes, stream_);
+    d_pxyzh_.ensure(n * sizeof(double4));
+    d_mvr_.ensure(n * sizeof(double4));
+    d_powh_.ensure(n * D * sizeof(double));
+    d_orig_.ensure(n * sizeof(int32_t));
+    launch_scatter_scene(d_raw_.as<sphray_particle>(), d_powh_raw_.as<double>(),
+                         d_idx2_.as<uint32_t>(), n, D, d_pxyzh_.as<double4>(), d_mvr_.as<double4>(),
+                         d_powh_.as<double>(), d_orig_.as<int32_t>(), stream_);
+    CUDA_OK(cudaStreamSynchronize(stream_));
+}
+
+namespace {
+// TransferFunction::validate (raycast.hpp:316-324)
+void validate_tf(const sphray_tf_point* tf, size_t ntf) {
+    if (ntf == 0 || !tf) fail(SPHRAY_ERR_CONFIG, "transfer function: no control points");
+    for (size_t i = 0; i < ntf; ++i) {
+        if (tf[i].absorption < 0.0)
+            fail(SPHRAY_ERR_CONFIG, "transfer function: absorption must be nonnegative");
+        if (i > 0 && !(tf[i].value > tf[i - 1].value))
+            fail(SPHRAY_ERR_CONFIG, "transfer function: values must be strictly increasing");
+    }
+}
+
+// TransferFunction::sample(0).absorption (raycast.hpp:326-337)
+double tf_absorption_at_zero(const sphray_tf_point* p, size_t n) {
+    const double v = 0.0;
+    if (v <= p[0].value) return p[0].absorption;
+    if (v >= p[n - 1].value) return p[n - 1].absorption;
+    size_t i = 1;
+    while (p[i].value < v) ++i;
+    const double w = (v - p[i - 1].value) / (p[i].value - p[i - 1].value);
+    return p[i - 1].absorption + w * (p[i].absorption - p[i - 1].absorption);
+}
+
+int bits_for(uint64_t v) {
+    int b = 1;
+    while (b < 32 && (1ull << b) <= v) ++b;
+    return b;
+}
+
+constexpr size_t kSmemLimit = 227 * 1024;
+}  // namespace
+
+void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t ntf,
+                    const sphray_quanta& qc, const sphray_dataset_stats& ds,
+                    const sphray_render_options& opts, double* rgb_host,
+                    sphray_render_stats* out, Dumps* dumps) {
+    set_device();
+    const CamConst C = make_camera(cam);  // render_scene: cam.validate() (raycast.hpp:419)
+    validate_tf(tf, ntf);                 // raycast.hpp:420
+    if (!has_scene_) fail(SPHRAY_ERR_CONFIG, "no scene uploaded");
+    if (qc.int_width != 64)
+        fail(SPHRAY_ERR_CONFIG,
+             "the B200 path computes with int64 quanta (int_width 64); widths 32/128 are not "
+             "supported yet");
+    const int D = lut_.D, m = lut_.m;
+    const double step = opts.step > 0.0 ? opts.step : ds.h_r / 8.0;  // raycast.hpp:424
+    const int W = C.W, H = C.H;
+    const size_t npix = static_cast<size_t>(W) * H;
+    const int tiles_x = (W + kTile - 1) / kTile, tiles_y = (H + kTile - 1) / kTile;
+    const uint64_t ntiles = static_cast<uint64_t>(tiles_x) * tiles_y;
+    const uint64_t owned = (ntiles + nranks_ - 1 - rank_) / nranks_;
+    const uint64_t owned_max = (ntiles + nranks_ - 1) / nranks_;
+    const int n = static_cast<int>(n_);
+    cudaStream_t s = stream_;
+
+    // per-frame uploads: TF, pow(tau, d) (glibc, quantize.hpp:221)
+    d_tf_.ensure(ntf * 5 * sizeof(double));
+    CUDA_OK(cudaMemcpyAsync(d_tf_.p, tf, ntf * 5 * sizeof(double), cudaMemcpyHostToDevice, s));
+    double powtau[kMaxDegree];
+    for (int d = 1; d <= D; ++d) powtau[d - 1] = std::pow(qc.tau, d);
+    d_powtau_.ensure(sizeof(powtau));
+    CUDA_OK(cudaMemcpyAsync(d_powtau_.p, powtau, sizeof(powtau), cudaMemcpyHostToDevice, s));
+    d_stats_.ensure(kStatCount * 8);
+    CUDA_OK(cudaMemsetAsync(d_stats_.p, 0, kStatCount * 8, s));
+    CUDA_OK(cudaMemsetAsync(d_stats_.as<unsigned long long>() + kStatOverflowKey, 0xff, 8, s));
+    d_work_.ensure(16);
+    d_retry_count_.ensure(16);
+    d_dump_count_.ensure(16);
+    CUDA_OK(cudaMemsetAsync(d_dump_count_.p, 0, 16, s));
+
+    CUDA_OK(cudaEventRecord(ev0_, s));
+    // ---- binning: reference bbox -> (tile, front) keys -> radix sort
+    uint64_t entries = 0;
+    if (n > 0) {
+        d_bbox_.ensure(static_cast<size_t>(n) * sizeof(int4));
+        d_front_.ensure(static_cast<size_t>(n) * sizeof(float));
+        d_xy_.ensure(static_cast<size_t>(n) * 2 * D * sizeof(double));
+        d_counts_.ensure(static_cast<size_t>(n) * 4);
+        d_offsets_.ensure(static_cast<size_t>(n) * 4);
+        PrepParams pp{};
+        pp.cam = C;
+        pp.n = n;
+        pp.D = D;
+        pp.q = lut_.q;
+        pp.reach_scale = std::max(lut_.theta_max, lut_.q);
+        pp.pxyzh = d_pxyzh_.as<double4>();
+        pp.mvr = d_mvr_.as<double4>();
+        pp.powh = d_powh_.as<double>();
+        pp.powtau = d_powtau_.as<double>();
+        pp.sigma = qc.sigma;
+        pp.bbox = d_bbox_.as<int4>();
+        pp.front = d_front_.as<float>();
+        pp.xy = d_xy_.as<double>();
+        pp.counts = d_counts_.as<uint32_t>();
+        pp.tiles_x = tiles_x;
+        pp.rank = rank_;
+        pp.nranks = nranks_;
+        launch_prep(pp, s);
+        const size_t scan_b = cub_scan_bytes(n);
+        d_tmp_.ensure(scan_b);
+        cub_scan(d_counts_.as<uint32_t>(), d_offsets_.as<uint32_t>(), n, d_tmp_.p, d_tmp_.bytes, s);
+        uint32_t tail[2];
+        CUDA_OK(cudaMemcpyAsync(&tail[0], d_offsets_.as<uint32_t>() + (n - 1), 4, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaMemcpyAsync(&tail[1], d_counts_.as<uint32_t>() + (n - 1), 4, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        entries = static_cast<uint64_t>(tail[0]) + tail[1];
+        if (entries >= 0xffffffffull)
+            fail(SPHRAY_ERR_CAPACITY, "more than 2^32 (tile, particle) entries; shard over more ranks");
+        d_tile_begin_.ensure(owned_max * 4);
+        d_tile_end_.ensure(owned_max * 4);
+        CUDA_OK(cudaMemsetAsync(d_tile_begin_.p, 0, owned_max * 4, s));
+        CUDA_OK(cudaMemsetAsync(d_tile_end_.p, 0, owned_max * 4, s));
+        if (entries > 0) {
+            d_keys_.ensure(entries * 8);
+            d_keys2_.ensure(entries * 8);
+            d_vals_.ensure(entries * 4);
+            d_vals2_.ensure(entries * 4);
+            launch_emit(pp, d_offsets_.as<uint32_t>(), d_keys_.as<unsigned long long>(),
+                        d_vals_.as<uint32_t>(), s);
+            const int end_bit = 32 + bits_for(owned_max);
+            const size_t sb = cub_sort_bytes(entries, end_bit);
+            d_tmp_.ensure(sb);
+            cub_sort(d_keys_.as<unsigned long long>(), d_keys2_.as<unsigned long long>(),
+                     d_vals_.as<uint32_t>(), d_vals2_.as<uint32_t>(), entries, end_bit, d_tmp_.p,
+                     d_tmp_.bytes, s);
+            launch_tile_ranges(d_keys2_.as<unsigned long long>(), entries,
+                               d_tile_begin_.as<uint32_t>(), d_tile_end_.as<uint32_t>(), s);
+        }
+    } else {
+        d_tile_begin_.ensure(owned_max * 4);
+        d_tile_end_.ensure(owned_max * 4);
+        CUDA_OK(cudaMemsetAsync(d_tile_begin_.p, 0, owned_max * 4, s));
+        CUDA_OK(cudaMemsetAsync(d_tile_end_.p, 0, owned_max * 4, s));
+    }
+
+    // ---- output buffers
+    const bool packed = nranks_ > 1;
+    d_image_.ensure(npix * 3 * sizeof(double));
+    double* target = d_image_.as<double>();
+    if (packed) {
+        d_packed_.ensure(owned_max * kTileRays * 3 * sizeof(double));
+        CUDA_OK(cudaMemsetAsync(d_packed_.p, 0, owned_max * kTileRays * 3 * sizeof(double), s));
+        target = d_packed_.as<double>();
+    }
+
+    // ---- render: persistent warps, one ray each at a time
+    FrameParams P{};
+    P.cam = C;
+    P.Q.lut_rows = d_lut_.as<double>();
+    P.Q.lut_stride = lut_.m + lut_.nj;
+    P.Q.lut_N = lut_.N;
+    P.Q.lut_dl = lut_.delta_lambda;
+    P.Q.q = lut_.q;
+    P.Q.K = lut_.K;
+    P.Q.m = lut_.m;
+    P.Q.tau = qc.tau;
+    P.Q.sigma = qc.sigma;
+    P.n = n;
+    P.pxyzh = d_pxyzh_.as<double4>();
+    P.xy = d_xy_.as<double>();
+    P.bbox = d_bbox_.as<int4>();
+    P.front = d_front_.as<float>();
+    P.orig = d_orig_.as<int32_t>();
+    P.cand = d_vals2_.as<uint32_t>();
+    P.tile_begin = d_tile_begin_.as<uint32_t>();
+    P.tile_end = d_tile_end_.as<uint32_t>();
+    P.tiles_x = tiles_x;
+    P.tiles_y = tiles_y;
+    P.rank = rank_;
+    P.nranks = nranks_;
+    P.tf = d_tf_.as<double>();
+    P.ntf = static_cast<int>(ntf);
+    P.tf0_clear = tf_absorption_at_zero(tf, ntf) == 0.0;
+    P.step = step;
+    P.bg[0] = opts.background[0];
+    P.bg[1] = opts.background[1];
+    P.bg[2] = opts.background[2];
+    P.mode = opts.mode;
+    P.work_counter = d_work_.as<unsigned long long>();
+    P.total_work = owned * kTileRays;
+    P.rgb = target;
+    P.packed = packed;
+    P.stats = d_stats_.as<unsigned long long>();
+    P.dump_count = d_dump_count_.as<unsigned long long>();
+    d_retry_.ensure(npix * 4);
+    d_retry2_.ensure(npix * 4);
+    P.retry_list = d_retry_.as<uint32_t>();
+    P.retry_count = d_retry_count_.as<unsigned int>();
+    if (dumps) {
+        if (dumps->hits) {
+            const size_t c = std::max<size_t>(dumps->cap_hits, 1);
+            d_dump_hr_.ensure(c * 8);
+            d_dump_hp_.ensure(c * 8);
+            d_dump_hl_.ensure(c * 8);
+            d_dump_ht_.ensure(c * 8);
+            P.dump_cap_hits = dumps->cap_hits;
+            P.dump_hit_ray = d_dump_hr_.as<uint64_t>();
+            P.dump_hit_pidx = d_dump_hp_.as<int64_t>();
+            P.dump_hit_lam = d_dump_hl_.as<double>();
+            P.dump_hit_tchi = d_dump_ht_.as<double>();
+        }
+        if (dumps->pieces) {
+            const size_t c = std::max<size_t>(dumps->cap_pieces, 1);
+            d_dump_pr_.ensure(c * 8);
+            d_dump_pt_.ensure(c * 8);
+            d_dump_pa_.ensure(c * (D + 1) * 8);
+            P.dump_cap_pieces = dumps->cap_pieces;
+            P.dump_piece_ray = d_dump_pr_.as<uint64_t>();
+            P.dump_piece_t = d_dump_pt_.as<int64_t>();
+            P.dump_piece_a = d_dump_pa_.as<int64_t>();
+        }
+        P.mode = SPHRAY_MODE_EXACT;
+    }
+    int cap = opts.window > 0 ? std::min(opts.window, 65535) : 512;
+    int warps = 4;
+    size_t wb = warp_smem_bytes(D, cap, m);
+    while (warps > 1 && wb * warps > kSmemLimit) --warps;
+    if (wb * warps > kSmemLimit) fail(SPHRAY_ERR_CONFIG, "knot window does not fit shared memory");
+    P.cap = cap;
+    P.warp_bytes = static_cast<int>(wb);
+    int bps = max_blocks_per_sm(D, m, warps, wb * warps);
+    if (bps < 1) bps = 1;
+    CUDA_OK(cudaMemsetAsync(d_work_.p, 0, 8, s));
+    CUDA_OK(cudaMemsetAsync(d_retry_count_.p, 0, 8, s));
+    if (P.total_work > 0) launch_render(P, D, m, sm_count_ * bps, warps, s);
+
+    // ---- rays whose window overflowed: once more with the widest window
+    unsigned retry = 0;
+    CUDA_OK(cudaMemcpyAsync(&retry, d_retry_count_.p, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    if (retry > 0) {
+        int cap2 = 65535;
+        while (cap2 > cap && warp_smem_bytes(D, cap2, m) > kSmemLimit) cap2 = cap2 * 15 / 16;
+        if (cap2 <= cap) fail(SPHRAY_ERR_CAPACITY, "knot window cannot grow");
+        FrameParams P2 = P;
+        P2.cap = cap2;
+        P2.warp_bytes = static_cast<int>(warp_smem_bytes(D, cap2, m));
+        P2.ray_list = d_retry_.as<uint32_t>();
+        P2.total_work = retry;
+        P2.retry_list = d_retry2_.as<uint32_t>();
+        P2.retry_count = d_retry_count_.as<unsigned int>() + 1;
+        CUDA_OK(cudaMemsetAsync(d_work_.p, 0, 8, s));
+        int bps2 = max_blocks_per_sm(D, m, 1, P2.warp_bytes);
+        if (bps2 < 1) bps2 = 1;
+        launch_render(P2, D, m, std::min<int>(retry, sm_count_ * bps2), 1, s);
+        unsigned retry2 = 0;
+        CUDA_OK(cudaMemcpyAsync(&retry2, d_retry_count_.as<unsigned int>() + 1, 4,
+                                cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        if (retry2 > 0)
+            fail(SPHRAY_ERR_CAPACITY, std::to_string(retry2) + " rays exceed the widest knot window (" +
+                                          std::to_string(cap2) + " knots)");
+    }
+    // skipped_particles: counted once (rank 0), the particle set is replicated
+    if (rank_ == 0)
+        launch_reach(C, n, lut_.q, d_pxyzh_.as<double4>(), d_bbox_.as<int4>(),
+                     d_stats_.as<unsigned long long>() + kStatSkipped, s);
+
+    // ---- gather finished tiles over NCCL (image-tile sharding)
+    unsigned long long st[kStatCount];
+    if (packed && comm_) {
+        auto& a = nccl();
+        const size_t per_rank = owned_max * kTileRays * 3;
+        d_gather_.ensure(per_rank * nranks_ * sizeof(double));
+        nccl_ok(a.AllGather(d_packed_.p, d_gather_.p, per_rank, ncclDouble,
+                            static_cast<ncclComm_t>(comm_), s),
+                "ncclAllGather(tiles)");
+        launch_unpack(d_gather_.as<double>(), per_rank, nranks_, tiles_x, W, H, d_image_.as<double>(), s);
+        d_stats_all_.ensure(kStatCount * 8 * nranks_);
+        nccl_ok(a.AllGather(d_stats_.p, d_stats_all_.p, kStatCount, ncclUint64,
+                            static_cast<ncclComm_t>(comm_), s),
+                "ncclAllGather(stats)");
+        std::vector<unsigned long long> all(kStatCount * nranks_);
+        CUDA_OK(cudaMemcpyAsync(all.data(), d_stats_all_.p, all.size() * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaEventRecord(ev1_, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        for (int k = 0; k < kStatCount; ++k) st[k] = (k == kStatOverflowKey) ? ~0ull : 0ull;
+        for (int r = 0; r < nranks_; ++r)
+            for (int k = 0; k < kStatCount; ++k) {
+                const unsigned long long v = all[r * kStatCount + k];
+                if (k == kStatOverflowKey)
+                    st[k] = std::min(st[k], v);
+                else if (k == kStatMaxPending)
+                    st[k] = std::max(st[k], v);
+                else
+                    st[k] += v;
+            }
+    } else {
+        CUDA_OK(cudaMemcpyAsync(st, d_stats_.p, sizeof(st), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaEventRecord(ev1_, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+    }
+    float ms = 0.0f;
+    CUDA_OK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+
+    if (st[kStatOverflowKey] != ~0ull) {
+        // quantize_particle's OverflowError names the particle and ray (quantize.hpp:244-249)
+        const int64_t pidx = static_cast<int64_t>(st[kStatOverflowKey] >> 32);
+        const uint64_t ray = st[kStatOverflowKey] & 0xffffffffull;
+        fail(SPHRAY_ERR_OVERFLOW,
+             "quantize: integer overflow (particle " + std::to_string(pidx) + ", ray " +
+                 std::to_string(ray) + ")",
+             pidx, ray);
+    }
+    if (st[kStatRays] > 0 && !(step > 0.0)) fail(SPHRAY_ERR_CONFIG, "composite: step must be positive");
+
+    if (rgb_host) {
+        if (packed && !comm_)  // shard without communicator: this rank's packed tiles
+            CUDA_OK(cudaMemcpyAsync(rgb_host, d_packed_.p, owned_max * kTileRays * 3 * sizeof(double),
+                                    cudaMemcpyDeviceToHost, s));
+        else
+            CUDA_OK(cudaMemcpyAsync(rgb_host, d_image_.p, npix * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+    }
+    if (dumps) {
+        unsigned long long dc[2];
+        CUDA_OK(cudaMemcpy(dc, d_dump_count_.p, 16, cudaMemcpyDeviceToHost));
+        dumps->n_hits = dc[0];
+        dumps->n_pieces = dc[1];
+        if (dumps->hits && dumps->cap_hits) {
+            const size_t k = std::min<size_t>(dc[0], dumps->cap_hits);
+            dumps->hit_ray.resize(k);
+            dumps->hit_pidx.resize(k);
+            dumps->hit_lam.resize(k);
+            dumps->hit_tchi.resize(k);
+            CUDA_OK(cudaMemcpy(dumps->hit_ray.data(), d_dump_hr_.p, k * 8, cudaMemcpyDeviceToHost));
+            CUDA_OK(cudaMemcpy(dumps->hit_pidx.data(), d_dump_hp_.p, k * 8, cudaMemcpyDeviceToHost));
+            CUDA_OK(cudaMemcpy(dumps->hit_lam.data(), d_dump_hl_.p, k * 8, cudaMemcpyDeviceToHost));
+            CUDA_OK(cudaMemcpy(dumps->hit_tchi.data(), d_dump_ht_.p, k * 8, cudaMemcpyDeviceToHost));
+        }
+        if (dumps->pieces && dumps->cap_pieces) {
+            const size_t k = std::min<size_t>(dc[1], dumps->cap_pieces);
+            dumps->piece_ray.resize(k);
+            dumps->piece_t.resize(k);
+            dumps->piece_a.resize(k * (D + 1));
+            CUDA_OK(cudaMemcpy(dumps->piece_ray.data(), d_dump_pr_.p, k * 8, cudaMemcpyDeviceToHost));
+            CUDA_OK(cudaMemcpy(dumps->piece_t.data(), d_dump_pt_.p, k * 8, cudaMemcpyDeviceToHost));
+            CUDA_OK(cudaMemcpy(dumps->piece_a.data(), d_dump_pa_.p, k * (D + 1) * 8, cudaMemcpyDeviceToHost));
+        }
+    }
+    if (out) {
+        sphray_render_stats o{};
+        o.particles = n_;
+        o.skipped_particles = st[kStatSkipped];
+        o.knots = st[kStatKnots];
+        o.rays_touched = st[kStatRays];
+        o.int_ops = st[kStatIntOps];
+        o.residual_failures = st[kStatResidual];
+        o.step = step;
+        o.hits = st[kStatHits];
+        o.candidates = entries;
+        o.window_retries = retry;
+        o.max_window = st[kStatMaxPending];
+        o.device_ms = ms;
+        *out = o;
+    }
+}
+
+void Engine::quantize_hits(const sphray_particle* ps, size_t nhits, const double* tchi,
+                           const double* lam, const sphray_lut_view& lutv, const sphray_quanta& qc,
+                           int64_t* knot_t, int64_t* knot_b, int32_t* knot_count) {
+    set_device();
+    const LutHost L = make_lut(lutv);
+    if (nhits == 0) return;
+    const int D = L.D, KN = L.K + 1;
+    std::vector<double> powh(nhits * D);
+    particle_powers(ps, nhits, D, powh.data());
+    double powtau[kMaxDegree];
+    for (int d = 1; d <= D; ++d) powtau[d - 1] = std::pow(qc.tau, d);
+    DevBuf lut, dps, dpw, dpt, dtc, dla, dkt, dkb, dkc;
+    lut.ensure(L.rows.size() * 8);
+    dps.ensure(nhits * sizeof(sphray_particle));
+    dpw.ensure(powh.size() * 8);
+    dpt.ensure(sizeof(powtau));
+    dtc.ensure(nhits * 8);
+    dla.ensure(nhits * 8);
+    dkt.ensure(nhits * KN * 8);
+    dkb.ensure(nhits * KN * (D + 1) * 8);
+    dkc.ensure(nhits * 4);
+    CUDA_OK(cudaMemcpy(lut.p, L.rows.data(), L.rows.size() * 8, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(dps.p, ps, nhits * sizeof(sphray_particle), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(dpw.p, powh.data(), powh.size() * 8, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(dpt.p, powtau, sizeof(powtau), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(dtc.p, tchi, nhits * 8, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(dla.p, lam, nhits * 8, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemset(dkt.p, 0, nhits * KN * 8));
+    CUDA_OK(cudaMemset(dkb.p, 0, nhits * KN * (D + 1) * 8));
+    QuantParams Q{};
+    Q.lut_rows = lut.as<double>();
+    Q.lut_stride = L.m + L.nj;
+    Q.lut_N = L.N;
+    Q.lut_dl = L.delta_lambda;
+    Q.q = L.q;
+    Q.K = L.K;
+    Q.m = L.m;
+    Q.tau = qc.tau;
+    Q.sigma = qc.sigma;
+    launch_quantize_hits(Q, D, dps.as<sphray_particle>(), dpw.as<double>(), dpt.as<double>(), nhits,
+                         dtc.as<double>(), dla.as<double>(), dkt.as<int64_t>(), dkb.as<int64_t>(),
+                         dkc.as<int32_t>(), stream_);
+    CUDA_OK(cudaStreamSynchronize(stream_));
+    CUDA_OK(cudaMemcpy(knot_t, dkt.p, nhits * KN * 8, cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(knot_b, dkb.p, nhits * KN * (D + 1) * 8, cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(knot_count, dkc.p, nhits * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < nhits; ++i)
+        if (knot_count[i] < 0)
+            fail(SPHRAY_ERR_OVERFLOW, "quantize: integer overflow (hit " + std::to_string(i) + ")",
+                 static_cast<int64_t>(i), 0);
+}
+
+}  // namespace sphray_b200

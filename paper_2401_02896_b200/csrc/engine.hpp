@@ -1,0 +1,96 @@
+// engine.hpp -- the device-resident renderer behind the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "host.hpp"
+#include "render.cuh"
+
+namespace sphray_b200 {
+
+// Grow-only device allocation.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t b);
+    void release();
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+    ~DevBuf() { release(); }
+};
+
+struct HostPinned {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t b);
+    ~HostPinned();
+};
+
+struct Dumps {
+    bool hits = false, pieces = false;
+    size_t cap_hits = 0, cap_pieces = 0;
+    // results (host)
+    uint64_t n_hits = 0, n_pieces = 0;
+    std::vector<uint64_t> hit_ray;
+    std::vector<int64_t> hit_pidx;
+    std::vector<double> hit_lam, hit_tchi;
+    std::vector<uint64_t> piece_ray;
+    std::vector<int64_t> piece_t, piece_a;
+};
+
+struct FrameOut {
+    sphray_render_stats stats{};
+};
+
+class Engine {
+   public:
+    explicit Engine(int device);
+    ~Engine();
+
+    void init_comm(int rank, int nranks, const uint8_t id[128]);
+    void set_shard(int rank, int nranks);
+    void upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_view& lut);
+    // Renders the resident scene.  rgb_host may be null (image stays on device).
+    void render(const sphray_camera& cam, const sphray_tf_point* tf, size_t ntf,
+                const sphray_quanta& qc, const sphray_dataset_stats& ds,
+                const sphray_render_options& opts, double* rgb_host, sphray_render_stats* out,
+                Dumps* dumps);
+    void quantize_hits(const sphray_particle* ps, size_t nhits, const double* tchi,
+                       const double* lam, const sphray_lut_view& lut, const sphray_quanta& qc,
+                       int64_t* knot_t, int64_t* knot_b, int32_t* knot_count);
+    const double* device_image() const { return d_image_.as<double>(); }
+    bool has_scene() const { return has_scene_; }
+    int rank() const { return rank_; }
+    int nranks() const { return nranks_; }
+
+   private:
+    void set_device() const;
+    int device_ = 0;
+    int sm_count_ = 0;
+    cudaStream_t stream_ = nullptr;
+    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    // communicator (tile gather)
+    int rank_ = 0, nranks_ = 1;
+    void* comm_ = nullptr;
+    // scene
+    bool has_scene_ = false;
+    size_t n_ = 0;
+    LutHost lut_;
+    DevBuf d_raw_, d_powh_raw_, d_codes_, d_codes2_, d_idx_, d_idx2_, d_tmp_;
+    DevBuf d_pxyzh_, d_mvr_, d_powh_, d_orig_, d_lut_;
+    // frame
+    DevBuf d_bbox_, d_front_, d_xy_, d_counts_, d_offsets_, d_keys_, d_keys2_, d_vals_, d_vals2_;
+    DevBuf d_tile_begin_, d_tile_end_, d_tf_, d_powtau_, d_image_, d_packed_, d_gather_;
+    DevBuf d_stats_, d_work_, d_retry_, d_retry2_, d_retry_count_;
+    DevBuf d_dump_count_, d_dump_hr_, d_dump_hp_, d_dump_hl_, d_dump_ht_, d_dump_pr_, d_dump_pt_,
+        d_dump_pa_, d_stats_all_;
+    HostPinned h_stage_;
+    std::vector<double> h_powh_;
+};
+
+}  // namespace sphray_b200

@@ -1,0 +1,475 @@
+// host.cpp -- host-side pieces of the path (see host.hpp).
+#include "host.hpp"
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <numbers>
+#include <random>
+#include <stdexcept>
+#include <thread>
+
+namespace sphray_b200 {
+
+void fail(sphray_status code, const std::string& msg, int64_t pidx, uint64_t ray) {
+    throw ThrownError(code, msg, pidx, ray);
+}
+
+int host_threads() {
+    if (const char* env = std::getenv("SPHRAY_THREADS")) {
+        const int v = std::atoi(env);
+        if (v >= 1) return v;
+    }
+    const unsigned hw = std::thread::hardware_concurrency();
+    return hw ? static_cast<int>(hw) : 1;
+}
+
+template <class F>
+static void parallel_chunks(size_t n, F&& fn) {
+    const int T = std::max(1, std::min<int>(host_threads(), static_cast<int>((n + 65535) / 65536)));
+    if (T <= 1) {
+        fn(size_t{0}, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const size_t chunk = (n + T - 1) / T;
+    for (int t = 0; t < T; ++t) {
+        const size_t lo = t * chunk, hi = std::min(n, lo + chunk);
+        if (lo >= hi) break;
+        pool.emplace_back([&, lo, hi] { fn(lo, hi); });
+    }
+    for (auto& th : pool) th.join();
+}
+
+// ---------------------------------------------------------------------------
+// Vec3 arithmetic in the reference's operation order (raycast.hpp:17-35).
+namespace {
+struct V3 {
+    double x, y, z;
+};
+inline V3 add(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+inline V3 sub(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+inline double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+inline V3 cross(V3 a, V3 o) {
+    return {a.y * o.z - a.z * o.y, a.z * o.x - a.x * o.z, a.x * o.y - a.y * o.x};
+}
+inline V3 scale(V3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+inline double norm(V3 a) { return std::sqrt(dot(a, a)); }
+inline V3 normalized(V3 a) {
+    const double n = norm(a);
+    if (!(n > 0.0)) fail(SPHRAY_ERR_CONFIG, "cannot normalize a zero vector");
+    return scale(a, 1.0 / n);
+}
+inline V3 v3(const double* p) { return {p[0], p[1], p[2]}; }
+inline void put(double* o, V3 v) {
+    o[0] = v.x;
+    o[1] = v.y;
+    o[2] = v.z;
+}
+}  // namespace
+
+CamConst make_camera(const sphray_camera& c) {
+    // Camera::validate, raycast.hpp:59-68
+    if (c.width < 1 || c.height < 1) fail(SPHRAY_ERR_CONFIG, "camera: resolution must be positive");
+    if (!(c.far_plane > c.near_plane))
+        fail(SPHRAY_ERR_CONFIG, "camera: far plane must lie beyond near");
+    if (c.mode != 0 && c.mode != 1) fail(SPHRAY_ERR_CONFIG, "camera: unknown mode");
+    if (c.mode == 1 && !(c.fov_deg > 0.0 && c.fov_deg < 180.0))
+        fail(SPHRAY_ERR_CONFIG, "camera: field of view must be inside (0, 180) degrees");
+    if (c.mode == 0 && !(c.ortho_height > 0.0))
+        fail(SPHRAY_ERR_CONFIG, "camera: orthographic height must be positive");
+    const V3 fwd = normalized(sub(v3(c.look_at), v3(c.position)));  // raycast.hpp:70
+    const V3 r0 = cross(fwd, v3(c.up));                                 // raycast.hpp:72
+    if (!(norm(r0) > 1e-12)) fail(SPHRAY_ERR_CONFIG, "camera: up is parallel to view direction");
+    const V3 right = normalized(r0);
+    const V3 upv = cross(right, fwd);  // raycast.hpp:76
+
+    CamConst k{};
+    k.mode = c.mode;
+    k.W = c.width;
+    k.H = c.height;
+    put(k.pos, v3(c.position));
+    put(k.fwd, fwd);
+    put(k.right, right);
+    put(k.upv, upv);
+    k.aspect = static_cast<double>(c.width) / c.height;
+    k.hw = 0.5 * c.ortho_height * k.aspect;
+    k.hh = 0.5 * c.ortho_height;
+    k.two_hw = 2 * k.hw;
+    k.two_hh = 2 * k.hh;
+    k.th = std::tan(c.fov_deg * std::numbers::pi / 360.0);
+    k.th_aspect = k.th * k.aspect;
+    k.near_plane = c.near_plane;
+    k.far_plane = c.far_plane;
+    return k;
+}
+
+// ---------------------------------------------------------------------------
+void validate_approx(int K, int D) {
+    if (K < 1 || K > kMaxPieces) fail(SPHRAY_ERR_CONFIG, "K must be in [1, 8]");
+    if (D < 1 || D > kMaxDegree) fail(SPHRAY_ERR_CONFIG, "D must be in [1, 6]");
+}
+
+LutHost make_lut(const sphray_lut_view& v) {
+    validate_approx(v.K, v.D);
+    if (!(v.q > 0.0)) fail(SPHRAY_ERR_IO, "lut: invalid support radius");
+    if (v.N < 1) fail(SPHRAY_ERR_NUMERIC, "lut: empty table");
+    if (!v.records) fail(SPHRAY_ERR_CONFIG, "lut: no records");
+    LutHost L;
+    L.q = v.q;
+    L.K = v.K;
+    L.D = v.D;
+    L.N = v.N;
+    L.m = (v.K + 1) / 2;  // positive_knot_count, approx.hpp:39
+    // basis_index_set, approx.hpp:44-54
+    for (int k = 1; k <= L.m; ++k)
+        for (int d = 1; d <= v.D; ++d) {
+            if (v.K % 2 == 1 && k == 1 && d % 2 == 1) continue;
+            L.idx_k.push_back(k);
+            L.idx_d.push_back(d);
+        }
+    L.nj = static_cast<int>(L.idx_k.size());
+    L.delta_lambda = v.q / static_cast<double>(v.N);
+    const int rec = 2 + L.m + L.nj;
+    L.rows.resize(static_cast<size_t>(v.N) * (L.m + L.nj));
+    double prev = -1.0;
+    for (int i = 0; i < v.N; ++i) {
+        const double* r = v.records + static_cast<size_t>(i) * rec;
+        L.lambda.push_back(r[0]);
+        L.error.push_back(r[1]);
+        if (!(r[0] > prev)) fail(SPHRAY_ERR_IO, "lut: distances not ascending");
+        prev = r[0];
+        for (int j = 0; j < L.m + L.nj; ++j)
+            L.rows[static_cast<size_t>(i) * (L.m + L.nj) + j] = r[2 + j];
+        for (int k = 0; k < L.m; ++k) L.theta_max = std::max(L.theta_max, std::fabs(r[2 + k]));
+    }
+    return L;
+}
+
+// ---------------------------------------------------------------------------
+// lut.hpp:100-168 in real arithmetic, as reconstruct_entry uses it.
+namespace {
+const long long kBinom[7][7] = {{1, 0, 0, 0, 0, 0, 0},  {1, 1, 0, 0, 0, 0, 0},
+                                {1, 2, 1, 0, 0, 0, 0},  {1, 3, 3, 1, 0, 0, 0},
+                                {1, 4, 6, 4, 1, 0, 0},  {1, 5, 10, 10, 5, 1, 0},
+                                {1, 6, 15, 20, 15, 6, 1}};
+
+struct DKnot {
+    double pos;
+    double b[kMaxDegree + 1];
+};
+
+std::vector<DKnot> mirror_closure_real(const double* pos /* m+1 */,
+                                       const double (*bpos)[kMaxDegree + 1], int m, int K,
+                                       int D) {
+    double bneg[kMaxM][kMaxDegree + 1] = {};
+    for (int k = 1; k <= m; ++k)
+        for (int d = 0; d <= D; ++d)
+            bneg[m - k][d] = (d % 2 == 1) ? bpos[k - 1][d] : -bpos[k - 1][d];
+    auto offset = [&](int k) { return pos[k] - pos[0]; };
+    double center[kMaxDegree + 1] = {};
+    if (K % 2 == 0) {
+        for (int d = 1; d <= D; d += 2) {
+            double acc = 0.0;
+            for (int k = 1; k <= m; ++k) {
+                const double off = offset(k);
+                double pw = 1.0;
+                for (int j = d; j <= D; ++j) {
+                    acc += static_cast<double>(kBinom[j][d]) * bneg[m - k][j] * pw;
+                    if (j < D) pw = pw * off;
+                }
+            }
+            center[d] = -(acc + acc);
+        }
+    } else {
+        for (int d = (D % 2 == 1 ? D : D - 1); d >= 1; d -= 2) {
+            double acc = 0.0;
+            for (int k = 2; k <= m; ++k) acc += bneg[m - k][d];
+            for (int k = 1; k <= m; ++k) {
+                const double off = offset(k);
+                double pw = off;
+                for (int j = d + 1; j <= D; ++j) {
+                    acc += static_cast<double>(kBinom[j][d]) * bneg[m - k][j] * pw;
+                    if (j < D) pw = pw * off;
+                }
+            }
+            bneg[m - 1][d] = -acc;
+        }
+    }
+    std::vector<DKnot> out;
+    for (int k = m; k >= 1; --k) {
+        DKnot kn{};
+        kn.pos = pos[0] + pos[0] - pos[k];
+        for (int d = 0; d <= kMaxDegree; ++d) kn.b[d] = bneg[m - k][d];
+        out.push_back(kn);
+    }
+    if (K % 2 == 0) {
+        DKnot kn{};
+        kn.pos = pos[0];
+        for (int d = 0; d <= kMaxDegree; ++d) kn.b[d] = center[d];
+        out.push_back(kn);
+    }
+    for (int k = 1; k <= m; ++k) {
+        DKnot kn{};
+        kn.pos = pos[k];
+        for (int d = 0; d <= D; ++d)
+            kn.b[d] = (d % 2 == 1) ? bneg[m - k][d] : -bneg[m - k][d];
+        out.push_back(kn);
+    }
+    return out;
+}
+}  // namespace
+
+// entry_amplitude + reconstruct_entry, lut.hpp:184-234.
+double entry_amplitude(const LutHost& L, int entry) {
+    const int m = L.m, D = L.D;
+    const double* row = &L.rows[static_cast<size_t>(entry) * (L.m + L.nj)];
+    double pos[kMaxM + 1] = {0.0};
+    for (int k = 1; k <= m; ++k) pos[k] = row[k - 1];
+    double bpos[kMaxM][kMaxDegree + 1] = {};
+    for (int i = 0; i < L.nj; ++i) bpos[L.idx_k[i] - 1][L.idx_d[i]] = row[m + i];
+    const auto knots = mirror_closure_real(pos, bpos, m, L.K, D);
+
+    std::vector<double> positions;
+    std::vector<std::array<double, kMaxDegree + 1>> local;
+    std::array<double, kMaxDegree + 1> a{};
+    double prev = 0.0;
+    for (size_t i = 0; i < knots.size(); ++i) {
+        if (i > 0) {
+            const double dt = knots[i].pos - prev;
+            std::array<double, kMaxDegree + 1> next{};
+            for (int d = 0; d <= D; ++d) {
+                double acc = knots[i].b[d];
+                double pw = 1.0;
+                for (int j = d; j <= D; ++j) {
+                    acc += static_cast<double>(kBinom[j][d]) * a[j] * pw;
+                    pw *= dt;
+                }
+                next[d] = acc;
+            }
+            a = next;
+        } else {
+            for (int d = 0; d <= kMaxDegree; ++d) a[d] = knots[i].b[d];
+        }
+        prev = knots[i].pos;
+        positions.push_back(knots[i].pos);
+        local.push_back(a);
+    }
+    auto eval_local = [&](size_t i, double x) {
+        double r = 0.0;
+        for (int d = D; d >= 0; --d) r = r * x + local[i][d];  // Polynomial::eval, n = D+1
+        return r;
+    };
+    auto evaluate = [&](double t) {
+        if (positions.empty() || t < positions.front() || t >= positions.back()) return 0.0;
+        size_t i = 0;
+        while (i + 1 < positions.size() && t >= positions[i + 1]) ++i;
+        return eval_local(i, t - positions[i]);
+    };
+    double amp = 0.0;
+    for (size_t i = 0; i + 1 < positions.size(); ++i)
+        for (int s = 0; s <= 32; ++s) {
+            const double t = positions[i] + (positions[i + 1] - positions[i]) * s / 32.0;
+            amp = std::max(amp, std::abs(evaluate(t)));
+        }
+    return amp;
+}
+
+// ---------------------------------------------------------------------------
+namespace {
+double median(std::vector<double> v) {  // quantize.hpp:118-122
+    std::sort(v.begin(), v.end());
+    const size_t n = v.size();
+    return n % 2 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
+}
+}  // namespace
+
+// dataset_stats, quantize.hpp:129-165.
+sphray_dataset_stats dataset_stats(const sphray_particle* ps, size_t n, const LutHost& L,
+                                   double clustering_factor) {
+    if (n == 0) fail(SPHRAY_ERR_CONFIG, "dataset_stats: empty particle set");
+    if (!(clustering_factor > 0.0))
+        fail(SPHRAY_ERR_CONFIG, "dataset_stats: clustering factor must be positive");
+    std::vector<double> mass(n), density(n), h(n), value(n);
+    double phi_max = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        const auto& p = ps[i];
+        if (!(p.h > 0.0) || !(p.density > 0.0))
+            fail(SPHRAY_ERR_CONFIG,
+                 "dataset_stats: particles need positive smoothing radius and density");
+        mass[i] = p.mass;
+        density[i] = p.density;
+        h[i] = p.h;
+        value[i] = p.value;
+        phi_max = std::max(phi_max, std::abs(p.mass * p.value / (p.density * p.h * p.h * p.h)));
+    }
+    sphray_dataset_stats s{};
+    s.mass_r = median(std::move(mass));
+    s.density_r = median(std::move(density));
+    s.h_r = median(std::move(h));
+    s.value_r = median(std::move(value));
+    s.phi_repr = s.mass_r * s.value_r / (s.density_r * s.h_r * s.h_r * s.h_r);
+    s.clustering_factor = clustering_factor;
+    s.count = n;
+    double amp = 0.0;
+    for (int e = 0; e < L.N; ++e) amp = std::max(amp, entry_amplitude(L, e));
+    s.a_max = clustering_factor * phi_max * amp;
+    return s;
+}
+
+// quantization_error_slope / optimal_tau / choose_quanta, quantize.hpp:55-183.
+namespace {
+double order_weight(double q, int d) {
+    return 2.0 * std::pow(q, 2 * d + 3) / ((2 * d + 1) * (2 * d + 3));
+}
+double slope(int D, double kappa, double kappa_prime, double q, double tau, double sigma) {
+    double s = 2.0 * kappa_prime * kappa_prime * tau;
+    for (int d = 1; d <= D; ++d)
+        s -= 2.0 * d * order_weight(q, d) * sigma * sigma / std::pow(tau, 2 * d + 1);
+    return s / (16.0 * kappa * kappa);
+}
+double optimal_tau(int D, double kappa, double kappa_prime, double q, double sigma) {
+    if (!(sigma > 0.0))
+        fail(SPHRAY_ERR_CONFIG,
+             "optimal_tau: sigma must be positive (a zero value quantum drives tau to zero)");
+    double lo = 1e-12, hi = 1e12;
+    while (slope(D, kappa, kappa_prime, q, lo, sigma) > 0.0 && lo > 1e-300) lo *= 1e-3;
+    while (slope(D, kappa, kappa_prime, q, hi, sigma) < 0.0 && hi < 1e300) hi *= 1e3;
+    for (int it = 0; it < 300 && hi > lo * (1.0 + 1e-15); ++it) {
+        const double mid = std::sqrt(lo * hi);
+        if (slope(D, kappa, kappa_prime, q, mid, sigma) > 0.0)
+            hi = mid;
+        else
+            lo = mid;
+    }
+    return std::sqrt(lo * hi);
+}
+}  // namespace
+
+sphray_quanta choose_quanta(const LutHost& L, const sphray_dataset_stats& ds, int width,
+                            double kappa, double kappa_prime) {
+    if (width != 32 && width != 64 && width != 128)
+        fail(SPHRAY_ERR_CONFIG, "int width must be one of 32, 64, 128");
+    if (!(ds.a_max > 0.0)) fail(SPHRAY_ERR_CONFIG, "choose_quanta: a_max must be positive");
+    if (!(ds.phi_repr > 0.0))
+        fail(SPHRAY_ERR_CONFIG,
+             "choose_quanta: representative contribution factor must be positive");
+    if (!(ds.h_r > 0.0))
+        fail(SPHRAY_ERR_CONFIG, "choose_quanta: representative smoothing radius must be positive");
+    sphray_quanta qc{};
+    qc.int_width = width;
+    qc.sigma = ds.a_max / (std::ldexp(1.0, width - 1) - 1.0);  // int_max_double, int_ops.hpp:45
+    qc.tau = optimal_tau(L.D, kappa, kappa_prime, L.q, qc.sigma / ds.phi_repr) * ds.h_r;
+    return qc;
+}
+
+void particle_powers(const sphray_particle* ps, size_t n, int D, double* out) {
+    parallel_chunks(n, [&](size_t lo, size_t hi) {
+        double last_h = std::nan(""), last[kMaxDegree] = {};
+        for (size_t i = lo; i < hi; ++i) {
+            const double h = ps[i].h;
+            if (!(h == last_h)) {
+                for (int d = 1; d <= D; ++d) last[d - 1] = std::pow(h, d + 3);  // quantize.hpp:222
+                last_h = h;
+            }
+            for (int d = 0; d < D; ++d) out[i * D + d] = last[d];
+        }
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic scenes.
+size_t scene_default_count(int config) {
+    switch (config) {
+        case 1: return 100000;
+        case 2: return 1000000;
+        case 3: return 16777216;
+        case 4: return 4194304;
+        case 5: return 100000000;
+    }
+    return 0;
+}
+
+namespace {
+void blob(size_t n, uint64_t seed, double h, sphray_particle* out) {
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> nd(0.0, 1.0);
+    const double mass = 1.0 / static_cast<double>(n);
+    for (size_t i = 0; i < n; ++i) {
+        const double x = nd(rng), y = nd(rng), z = nd(rng);
+        const double rho = std::exp(-(x * x + y * y + z * z) / 2.0) + 0.05;
+        out[i] = {x, y, z, mass, rho, h, rho};
+    }
+}
+
+// 256 Plummer halos + 10 % uniform background in [-3,3]^3; h from the
+// analytic mixture density: h = 1.2 (m / rho_model)^(1/3).
+void clustered(size_t n, uint64_t seed, sphray_particle* out) {
+    constexpr int kHalos = 256;
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> U(0.0, 1.0);
+    std::normal_distribution<double> nd(0.0, 1.0);
+    double cx[kHalos], cy[kHalos], cz[kHalos], a[kHalos], w[kHalos];
+    double wsum = 0.0;
+    for (int i = 0; i < kHalos; ++i) {
+        do {
+            cx[i] = 0.9 * nd(rng);
+            cy[i] = 0.9 * nd(rng);
+            cz[i] = 0.9 * nd(rng);
+        } while (std::fabs(cx[i]) > 2.5 || std::fabs(cy[i]) > 2.5 || std::fabs(cz[i]) > 2.5);
+        a[i] = std::exp(std::log(0.02) + (std::log(0.3) - std::log(0.02)) * U(rng));
+        w[i] = std::min(100.0, std::pow(1.0 - U(rng), -1.0 / 1.5));  // Pareto alpha = 1.5
+        wsum += w[i];
+    }
+    for (int i = 0; i < kHalos; ++i) w[i] = 0.9 * w[i] / wsum;  // mass fractions
+    const double mass = 1.0 / static_cast<double>(n);
+    size_t k = 0;
+    for (int i = 0; i < kHalos && k < n; ++i) {
+        const size_t cnt = std::min(n - k, static_cast<size_t>(w[i] * static_cast<double>(n)));
+        for (size_t j = 0; j < cnt; ++j, ++k) {
+            double r;
+            do {
+                const double u = std::max(U(rng), 1e-300);
+                r = a[i] / std::sqrt(std::pow(u, -2.0 / 3.0) - 1.0);
+            } while (!(r < 15.0 * a[i]));
+            const double ct = 2.0 * U(rng) - 1.0, ph = 2.0 * std::numbers::pi * U(rng);
+            const double st = std::sqrt(std::max(0.0, 1.0 - ct * ct));
+            out[k] = {cx[i] + r * st * std::cos(ph), cy[i] + r * st * std::sin(ph), cz[i] + r * ct,
+                      mass, 0.0, 0.0, 0.0};
+        }
+    }
+    for (; k < n; ++k)
+        out[k] = {-3.0 + 6.0 * U(rng), -3.0 + 6.0 * U(rng), -3.0 + 6.0 * U(rng), mass, 0.0, 0.0, 0.0};
+    double norm[kHalos];
+    for (int i = 0; i < kHalos; ++i) norm[i] = w[i] * 3.0 / (4.0 * std::numbers::pi * a[i] * a[i] * a[i]);
+    const double bg = 0.1 / 216.0;
+    parallel_chunks(n, [&](size_t lo, size_t hi) {
+        for (size_t p = lo; p < hi; ++p) {
+            double rho = bg;
+            for (int i = 0; i < kHalos; ++i) {
+                const double dx = out[p].x - cx[i], dy = out[p].y - cy[i], dz = out[p].z - cz[i];
+                const double s = 1.0 + (dx * dx + dy * dy + dz * dz) / (a[i] * a[i]);
+                rho += norm[i] / (s * s * std::sqrt(s));
+            }
+            out[p].density = rho;
+            out[p].value = rho;
+            out[p].h = 1.2 * std::cbrt(mass / rho);
+        }
+    });
+}
+}  // namespace
+
+void generate_scene(int config, size_t n, uint64_t seed, sphray_particle* out) {
+    switch (config) {
+        case 1: blob(n, seed, n == 100000 ? 0.062 : 0.062 * std::cbrt(1e5 / n), out); return;
+        case 2: blob(n, seed, n == 1000000 ? 0.029 : 0.062 * std::cbrt(1e5 / n), out); return;
+        case 4: blob(n, seed, 0.062 * std::cbrt(1e5 / n), out); return;
+        case 3:
+        case 5: clustered(n, seed, out); return;
+    }
+    fail(SPHRAY_ERR_CONFIG, "unknown scene config " + std::to_string(config));
+}
+
+}  // namespace sphray_b200

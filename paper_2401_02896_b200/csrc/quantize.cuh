@@ -1,0 +1,171 @@
+// quantize.cuh -- quantize_particle<int64_t> (quantize.hpp:199-250) with the
+// integer mirror closure (lut.hpp:100-168), split in two phases so the render
+// kernel can allocate window slots between them:
+//   phase A (positions)    quantize.hpp:211-216, lut.hpp:147-166
+//   phase B (coefficients) quantize.hpp:218-242, lut.hpp:104-145
+// Checked<int64_t> semantics: wrapping arithmetic plus an overflow flag.
+#pragma once
+
+#include "device_math.cuh"
+#include "render.cuh"
+
+namespace sphray_b200 {
+namespace dev {
+
+__constant__ long long c_binom[7][7] = {{1, 0, 0, 0, 0, 0, 0},  {1, 1, 0, 0, 0, 0, 0},
+                                        {1, 2, 1, 0, 0, 0, 0},  {1, 3, 3, 1, 0, 0, 0},
+                                        {1, 4, 6, 4, 1, 0, 0},  {1, 5, 10, 10, 5, 1, 0},
+                                        {1, 6, 15, 20, 15, 6, 1}};
+
+template <int M>
+struct HitPositions {
+    static constexpr int KN = 2 * M + 1;
+    int64_t pos[M + 1];  // pos[0] centre, pos[k] positive knots
+    int64_t kpos[KN];       // emission order -m..-1, [0], 1..m (nondecreasing)
+    int nraw;               // emitted entries before the coincident merge
+    int nk;                 // distinct positions (knots actually emitted)
+    const double* row;      // LUT entry: m knots then |J| jumps
+};
+
+// Phase A.  Returns false when quantize_particle emits nothing (lam >= q,
+// quantize.hpp:204).
+template <int M>
+__device__ __forceinline__ bool quantize_positions(const QuantParams& Q, double h, double lam,
+                                                   double tchi, HitPositions<M>& hp,
+                                                   bool& ovf) {
+    hp.nraw = 0;
+    hp.nk = 0;
+#pragma unroll
+    for (int k = 0; k <= M; ++k) hp.pos[k] = 0;
+    if (!(lam < Q.q)) return false;
+    const int e = lut_index(lam, Q.lut_dl, Q.lut_N);
+    hp.row = Q.lut_rows + static_cast<size_t>(e) * Q.lut_stride;
+    hp.pos[0] = round_checked(ddiv(tchi, Q.tau), ovf);
+#pragma unroll
+    for (int k = 1; k <= M; ++k)
+        if (k <= M)
+            hp.pos[k] = cadd(hp.pos[0], round_checked(ddiv(dmul(h, hp.row[k - 1]), Q.tau), ovf), ovf);
+    const int64_t twice = cadd(hp.pos[0], hp.pos[0], ovf);
+#pragma unroll
+    for (int k = M; k >= 1; --k)
+        if (k <= M) hp.kpos[hp.nraw++] = csub(twice, hp.pos[k], ovf);  // lut.hpp:150
+    if ((Q.K & 1) == 0) hp.kpos[hp.nraw++] = hp.pos[0];
+#pragma unroll
+    for (int k = 1; k <= M; ++k)
+        if (k <= M) hp.kpos[hp.nraw++] = hp.pos[k];
+    hp.nk = 1;
+#pragma unroll
+    for (int q = 1; q < HitPositions<M>::KN; ++q)
+        if (q < hp.nraw && hp.kpos[q] != hp.kpos[q - 1]) ++hp.nk;
+    return true;
+}
+
+// Phase B.  X[0..D) = (pow(tau,d)*mass)*value, X[D..2D) = (sigma*density)*pow(h,d+3)
+// (quantize.hpp:221-222 with the libm parts precomputed on the host).
+// sink(o, t, b) receives distinct knot o (0..nk) with its D+1 jumps.
+template <int D, int M, class Sink>
+__device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double* X,
+                                              const HitPositions<M>& hp, bool& ovf,
+                                              Sink&& sink) {
+    constexpr int m = M;
+    int64_t negk[M][D + 1];  // negk[k-1] == bneg[m-k] of lut.hpp:106
+    int64_t center[D + 1];
+#pragma unroll
+    for (int k = 0; k < M; ++k)
+#pragma unroll
+        for (int d = 0; d <= D; ++d) negk[k][d] = 0;
+#pragma unroll
+    for (int d = 0; d <= D; ++d) center[d] = 0;
+    const int c1 = (Q.K & 1) ? D / 2 : D;  // index-set entries with k == 1 (approx.hpp:48-51)
+#pragma unroll
+    for (int k = 1; k <= M; ++k) {
+        if (k > M) continue;
+#pragma unroll
+        for (int d = 1; d <= D; ++d) {
+            int ii;
+            if (k == 1) {
+                if ((Q.K & 1) && (d & 1)) continue;
+                ii = (Q.K & 1) ? d / 2 - 1 : d - 1;
+            } else {
+                ii = c1 + (k - 2) * D + (d - 1);
+            }
+            const double raw = ddiv(dmul(X[d - 1], hp.row[m + ii]), X[D + d - 1]);
+            const int64_t bp = round_checked(raw, ovf);
+            negk[k - 1][d] = (d & 1) ? bp : cneg(bp, ovf);  // lut.hpp:107-109
+        }
+    }
+    if ((Q.K & 1) == 0) {
+        // even K: the centre knot carries the odd-order jumps (lut.hpp:118-130)
+#pragma unroll
+        for (int d = 1; d <= D; d += 2) {
+            int64_t acc = 0;
+#pragma unroll
+            for (int k = 1; k <= M; ++k) {
+                if (k > M) continue;
+                const int64_t off = csub(hp.pos[k], hp.pos[0], ovf);
+                int64_t pw = 1;
+#pragma unroll
+                for (int j = d; j <= D; ++j) {
+                    acc = cadd(acc, cmul(cmul(c_binom[j][d], negk[k - 1][j], ovf), pw, ovf), ovf);
+                    if (j < D) pw = cmul(pw, off, ovf);
+                }
+            }
+            center[d] = cneg(cadd(acc, acc, ovf), ovf);
+        }
+    } else {
+        // odd K: the innermost pair closes, descending odd d (lut.hpp:131-145)
+#pragma unroll
+        for (int d = (D % 2 == 1 ? D : D - 1); d >= 1; d -= 2) {
+            int64_t acc = 0;
+#pragma unroll
+            for (int k = 2; k <= M; ++k)
+                if (k <= m) acc = cadd(acc, negk[k - 1][d], ovf);
+#pragma unroll
+            for (int k = 1; k <= M; ++k) {
+                if (k > M) continue;
+                const int64_t off = csub(hp.pos[k], hp.pos[0], ovf);
+                int64_t pw = off;
+#pragma unroll
+                for (int j = d + 1; j <= D; ++j) {
+                    acc = cadd(acc, cmul(cmul(c_binom[j][d], negk[k - 1][j], ovf), pw, ovf), ovf);
+                    if (j < D) pw = cmul(pw, off, ovf);
+                }
+            }
+            negk[0][d] = cneg(acc, ovf);
+        }
+    }
+    // assembly (lut.hpp:147-166) with the coincident merge of quantize.hpp:229-242
+    int64_t cur[D + 1];
+#pragma unroll
+    for (int d = 0; d <= D; ++d) cur[d] = 0;
+    int o = 0, q = 0;
+    auto put = [&](const int64_t (&b)[D + 1]) {
+        if (q > 0 && hp.kpos[q] == hp.kpos[q - 1]) {
+#pragma unroll
+            for (int d = 0; d <= D; ++d) cur[d] = cadd(cur[d], b[d], ovf);
+        } else {
+            if (q > 0) sink(o++, hp.kpos[q - 1], cur);
+#pragma unroll
+            for (int d = 0; d <= D; ++d) cur[d] = b[d];
+        }
+        ++q;
+    };
+#pragma unroll
+    for (int k = M; k >= 1; --k) {
+        if (k > M) continue;
+        put(negk[k - 1]);
+    }
+    if ((Q.K & 1) == 0) put(center);
+#pragma unroll
+    for (int k = 1; k <= M; ++k) {
+        if (k > M) continue;
+        int64_t b[D + 1];
+#pragma unroll
+        for (int d = 0; d <= D; ++d) b[d] = (d & 1) ? negk[k - 1][d] : cneg(negk[k - 1][d], ovf);
+        put(b);
+    }
+    sink(o, hp.kpos[q - 1], cur);
+}
+
+}  // namespace dev
+}  // namespace sphray_b200

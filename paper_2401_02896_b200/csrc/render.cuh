@@ -1,0 +1,156 @@
+// render.cuh -- device-side parameter blocks and launchers shared by the
+// kernels (render.cu) and the engine (engine.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "host.hpp"
+
+namespace sphray_b200 {
+
+constexpr int kTileShift = 3;  // 8x8-pixel screen tiles
+constexpr int kTile = 1 << kTileShift;
+constexpr int kTileRays = kTile * kTile;
+constexpr int kHitQueue = 64;
+constexpr int kMaxJ = kMaxM * kMaxDegree;
+
+#ifdef __CUDACC__
+#define SPHRAY_HD __host__ __device__
+#else
+#define SPHRAY_HD
+#endif
+
+// Shared-memory bytes of one warp's knot window (layout: render_kernel.cuh carve()).
+SPHRAY_HD inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+SPHRAY_HD inline size_t warp_bytes_for(int D, int cap, int nb) {
+    size_t b = 0;
+    b += align16(sizeof(uint64_t) * (D + 1) * cap);
+    b += align16(sizeof(int64_t) * cap);
+    b += align16(sizeof(int64_t) * nb);
+    b += align16(sizeof(double) * kHitQueue * 2);
+    b += align16(sizeof(int32_t) * kHitQueue * 2);
+    b += align16(sizeof(uint16_t) * cap * 2);
+    b += align16(sizeof(uint16_t) * nb);
+    return b;
+}
+
+// LUT + quanta view used by quantization (lut.hpp:25-52, quantize.hpp:44-51).
+struct QuantParams {
+    const double* lut_rows;  // N * (m + nj)
+    int lut_stride, lut_N;
+    double lut_dl, q;
+    int K, m;
+    double tau, sigma;
+};
+
+// Per-frame constants of the render kernel.
+struct FrameParams {
+    CamConst cam;
+    QuantParams Q;
+    // scene (Morton-ordered SoA)
+    int n;
+    const double4* pxyzh;  // x, y, z, h
+    const double* xy;      // n * 2D: X_1..X_D, Y_1..Y_D   (quantize.hpp:221-222)
+    const int4* bbox;      // reference footprint bbox per particle (clipped)
+    const float* front;    // knot-position lower bound (world units, rounded down)
+    const int32_t* orig;   // original particle index
+    // binning
+    const uint32_t* cand;        // particle indices, sorted by (tile, front)
+    const uint32_t* tile_begin;  // per owned tile
+    const uint32_t* tile_end;
+    int tiles_x, tiles_y;
+    int rank, nranks;
+    // transfer function (raycast.hpp:313-338)
+    const double* tf;  // ntf * 5
+    int ntf;
+    int tf0_clear;  // tf.sample(0).absorption == 0: zero pieces are exact no-ops
+    double step;
+    double bg[3];
+    int mode;
+    // knot window
+    int cap;         // knot slots per warp
+    int warp_bytes;  // dynamic smem per warp
+    // work distribution
+    unsigned long long* work_counter;
+    uint64_t total_work;
+    const uint32_t* ray_list;  // retry pass: explicit ray ids (else tile-major)
+    uint32_t* retry_list;
+    unsigned int* retry_count;
+    // output
+    double* rgb;  // full image (packed == 0) or owned tiles, tile-major
+    int packed;
+    unsigned long long* stats;  // StatIndex
+    // validation dumps (optional)
+    unsigned long long* dump_count;  // [0] hits [1] pieces
+    uint64_t dump_cap_hits, dump_cap_pieces;
+    uint64_t* dump_hit_ray;
+    int64_t* dump_hit_pidx;
+    double* dump_hit_lam;
+    double* dump_hit_tchi;
+    uint64_t* dump_piece_ray;
+    int64_t* dump_piece_t;
+    int64_t* dump_piece_a;  // (D+1) per piece
+};
+
+enum StatIndex {
+    kStatKnots = 0,
+    kStatRays = 1,
+    kStatIntOps = 2,
+    kStatResidual = 3,
+    kStatHits = 4,
+    kStatMaxPending = 5,
+    kStatOverflowKey = 6,
+    kStatSkipped = 7,
+    kStatCount = 8
+};
+
+// Per-frame particle prep (view + quanta dependent).
+struct PrepParams {
+    CamConst cam;
+    int n, D;
+    double q, reach_scale;  // knot reach = h * reach_scale (largest LUT knot radius)
+    const double4* pxyzh;
+    const double4* mvr;    // mass, value, density
+    const double* powh;    // n*D: pow(h, d+3)
+    const double* powtau;  // D: pow(tau, d)
+    double sigma;
+    int4* bbox;
+    float* front;
+    double* xy;
+    uint32_t* counts;
+    int tiles_x, rank, nranks;
+};
+
+size_t warp_smem_bytes(int D, int cap, int m);
+int max_blocks_per_sm(int D, int m, int warps, size_t smem);
+void launch_render(const FrameParams& P, int D, int m, int blocks, int warps, cudaStream_t s);
+void launch_prep(const PrepParams& p, cudaStream_t s);
+void launch_emit(const PrepParams& p, const uint32_t* offsets, unsigned long long* keys,
+                 uint32_t* vals, cudaStream_t s);
+void launch_tile_ranges(const unsigned long long* keys, size_t m, uint32_t* begin, uint32_t* end,
+                        cudaStream_t s);
+void launch_reach(const CamConst& cam, int n, double q, const double4* pxyzh, const int4* bbox,
+                  unsigned long long* skipped, cudaStream_t s);
+void launch_unpack(const double* packed, size_t per_rank, int nranks, int tiles_x, int W, int H,
+                   double* out, cudaStream_t s);
+void launch_fill_bg(double* rgb, size_t npix, const double* bg, cudaStream_t s);
+void launch_morton(const sphray_particle* ps, size_t n, const double* lo, const double* inv,
+                   unsigned long long* codes, uint32_t* idx, cudaStream_t s);
+void launch_scatter_scene(const sphray_particle* ps, const double* powh_in, const uint32_t* perm,
+                          size_t n, int D, double4* pxyzh, double4* mvr, double* powh,
+                          int32_t* orig, cudaStream_t s);
+void launch_quantize_hits(const QuantParams& Q, int D, const sphray_particle* ps,
+                          const double* powh, const double* powtau, size_t nhits,
+                          const double* tchi, const double* lam, int64_t* knot_t,
+                          int64_t* knot_b, int32_t* knot_count, cudaStream_t s);
+
+size_t cub_scan_bytes(size_t n);
+void cub_scan(const uint32_t* in, uint32_t* out, size_t n, void* tmp, size_t bytes, cudaStream_t s);
+size_t cub_sort_bytes(size_t n, int end_bit);
+void cub_sort(const unsigned long long* kin, unsigned long long* kout, const uint32_t* vin,
+              uint32_t* vout, size_t n, int end_bit, void* tmp, size_t bytes, cudaStream_t s);
+
+}  // namespace sphray_b200

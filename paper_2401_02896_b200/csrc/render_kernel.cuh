@@ -1,0 +1,789 @@
+// render_kernel.cuh -- the per-ray render kernel (warp per ray) and the
+// explicit-hit quantization kernel, as templates over (D, m).  Each
+// render_d<D>.cu instantiates them for one degree so the 24 (D, m) variants
+// compile in parallel.  See render.cu for the reference mapping.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "device_math.cuh"
+#include "quantize.cuh"
+#include "render.cuh"
+
+namespace sphray_b200 {
+namespace rk {
+
+using namespace dev;
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T u = __shfl_up_sync(kFull, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+__device__ __forceinline__ int lower_bound64(const int64_t* a, int n, int64_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < x)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int upper_bound64(const int64_t* a, int n, int64_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] <= x)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// floor(front / tau) - 2: every knot of a not-yet-inserted candidate has
+// t >= this (front is a conservative bound, see dev::front_bound).
+__device__ __forceinline__ int64_t knot_floor(float front, double tau) {
+    const double v = floor(static_cast<double>(front) / tau) - 2.0;
+    if (!(v > -9.2e18)) return INT64_MIN;
+    if (!(v < 9.2e18)) return INT64_MAX;
+    return static_cast<int64_t>(v);
+}
+
+// TransferFunction::sample (raycast.hpp:326-337).
+__device__ __forceinline__ void tf_sample(const double* tf, int n, double v, double& r, double& g,
+                                          double& b, double& ab) {
+    if (v <= tf[0]) {
+        r = tf[1];
+        g = tf[2];
+        b = tf[3];
+        ab = tf[4];
+        return;
+    }
+    const double* last = tf + 5 * (n - 1);
+    if (v >= last[0]) {
+        r = last[1];
+        g = last[2];
+        b = last[3];
+        ab = last[4];
+        return;
+    }
+    int i = 1;
+    while (tf[5 * i] < v) ++i;
+    const double* A = tf + 5 * (i - 1);
+    const double* B = tf + 5 * i;
+    const double w = ddiv(dsub(v, A[0]), dsub(B[0], A[0]));
+    r = dadd(A[1], dmul(w, dsub(B[1], A[1])));
+    g = dadd(A[2], dmul(w, dsub(B[2], A[2])));
+    b = dadd(A[3], dmul(w, dsub(B[3], A[3])));
+    ab = dadd(A[4], dmul(w, dsub(B[4], A[4])));
+}
+
+// Warp bitonic sort of 32*R (t, slot) pairs held R per lane (blocked layout:
+// element e = lane*R + r).  Ascending in t; equal t may end in any order
+// (their jumps are summed).
+template <int R>
+__device__ __forceinline__ void bitonic_sort(int64_t (&t)[R], int (&s)[R], int lane) {
+#pragma unroll
+    for (int size = 2; size <= 32 * R; size <<= 1) {
+#pragma unroll
+        for (int stride = size / 2; stride >= R; stride >>= 1) {
+            const int ls = stride / R;
+            const bool asc = ((lane * R) & size) == 0;
+            const bool lower = (lane & ls) == 0;
+            const bool keep_min = lower == asc;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int64_t ot = __shfl_xor_sync(kFull, t[r], ls);
+                const int os = __shfl_xor_sync(kFull, s[r], ls);
+                const bool take = keep_min ? (ot < t[r]) : (ot > t[r]);
+                if (take) {
+                    t[r] = ot;
+                    s[r] = os;
+                }
+            }
+        }
+#pragma unroll
+        for (int stride = (size / 2 < R ? size / 2 : R / 2); stride >= 1; stride >>= 1) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if ((r & stride) == 0) {
+                    const int r2 = r | stride;
+                    const bool asc = (((lane * R) + r) & size) == 0;
+                    const bool sw = asc ? (t[r] > t[r2]) : (t[r] < t[r2]);
+                    if (sw) {
+                        const int64_t tt = t[r];
+                        t[r] = t[r2];
+                        t[r2] = tt;
+                        const int ss = s[r];
+                        s[r] = s[r2];
+                        s[r2] = ss;
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int M>
+struct Cfg {
+    static constexpr int KN = 2 * M + 1;
+    static constexpr int R = KN <= 8 ? 8 : 16;
+    static constexpr int NB = 32 * R;
+};
+
+struct WarpMem {
+    uint64_t* pool;  // (D+1) x cap, SoA: jumps while pending, merged coefficients once a piece
+    int64_t* pt;     // pending knot positions, sorted ascending
+    int64_t* nt;     // staging: sorted new knots / the pieces of a chunk
+    double* hq_lam;  // hit queue (candidate order)
+    double* hq_t;
+    int32_t* hq_c;
+    int32_t* hq_p;
+    uint16_t* ps;  // pending slots
+    uint16_t* fl;  // free slot stack
+    uint16_t* ns;  // staging slots
+};
+
+
+__device__ inline WarpMem carve(char* base, int D, int cap, int nb) {
+    WarpMem w;
+    char* p = base;
+    w.pool = reinterpret_cast<uint64_t*>(p);
+    p += align16(sizeof(uint64_t) * (D + 1) * cap);
+    w.pt = reinterpret_cast<int64_t*>(p);
+    p += align16(sizeof(int64_t) * cap);
+    w.nt = reinterpret_cast<int64_t*>(p);
+    p += align16(sizeof(int64_t) * nb);
+    w.hq_lam = reinterpret_cast<double*>(p);
+    w.hq_t = w.hq_lam + kHitQueue;
+    p += align16(sizeof(double) * kHitQueue * 2);
+    w.hq_c = reinterpret_cast<int32_t*>(p);
+    w.hq_p = w.hq_c + kHitQueue;
+    p += align16(sizeof(int32_t) * kHitQueue * 2);
+    w.ps = reinterpret_cast<uint16_t*>(p);
+    w.fl = w.ps + cap;
+    p += align16(sizeof(uint16_t) * cap * 2);
+    w.ns = reinterpret_cast<uint16_t*>(p);
+    return w;
+}
+
+// One warp renders one ray at a time.
+template <int D, int M>
+class RayWorker {
+   public:
+    using C = Cfg<M>;
+    const FrameParams& P;
+    WarpMem w;
+    int lane;
+    uint64_t ray_id = 0;
+    // warp-uniform ray state
+    int np = 0, nfree = 0;
+    uint64_t G[D + 1];  // running sum of jumps shifted to tref (mod 2^64)
+    int64_t tref = 0;
+    bool has_ref = false;
+    int64_t open_t = 0;  // last piece: its successor is not known yet
+    int open_slot = 0;
+    bool has_open = false;
+    double T = 1.0, Cr = 0.0, Cg = 0.0, Cb = 0.0;
+    bool term = false;
+    unsigned long long knots = 0, pieces = 0, hits = 0;
+    int max_pending = 0;
+
+    __device__ RayWorker(const FrameParams& p, WarpMem wm, int l) : P(p), w(wm), lane(l) {}
+
+    __device__ void reset() {
+        np = 0;
+        nfree = P.cap;
+        for (int i = lane; i < P.cap; i += 32) w.fl[i] = static_cast<uint16_t>(P.cap - 1 - i);
+#pragma unroll
+        for (int d = 0; d <= D; ++d) G[d] = 0;
+        tref = 0;
+        has_ref = false;
+        open_t = 0;
+        open_slot = 0;
+        has_open = false;
+        T = 1.0;
+        Cr = Cg = Cb = 0.0;
+        term = false;
+        knots = pieces = hits = 0;
+        max_pending = 0;
+        __syncwarp();
+    }
+
+    __device__ void free_slots(bool give, int slot) {
+        const unsigned m = __ballot_sync(kFull, give);
+        if (give) w.fl[nfree + __popc(m & lanemask_lt())] = static_cast<uint16_t>(slot);
+        nfree += __popc(m);
+        __syncwarp();
+    }
+
+    // Composite the pieces completed in this chunk: lane j (j < cp) takes the
+    // piece that starts at the previous piece (the carried open piece for
+    // j == 0) and ends at staged piece j -- composite(), raycast.hpp:356-381,
+    // distributed over samples rather than pieces so long gaps do not
+    // serialise one lane.
+    __device__ void composite_chunk(int cp) {
+        const bool have = lane < cp && (lane > 0 || has_open);
+        int64_t ts = 0, te = 0;
+        int slot = 0;
+        if (lane < cp) {
+            te = w.nt[lane];
+            if (lane == 0) {
+                ts = open_t;
+                slot = open_slot;
+            } else {
+                ts = w.nt[lane - 1];
+                slot = w.ns[lane - 1];
+            }
+        }
+        const int last_slot = __shfl_sync(kFull, lane < cp ? static_cast<int>(w.ns[lane]) : 0, cp - 1);
+        const int64_t last_t = __shfl_sync(kFull, te, cp - 1);
+
+        if (!term) {
+            int n = 0;
+            double lo = 0.0, dt = 0.0;
+            if (have) {
+                // [lo, hi] = [t_i tau, t_{i+1} tau] cut to [near, far]   (raycast.hpp:364-368)
+                const double a_lo = dmul(static_cast<double>(ts), P.Q.tau);
+                const double a_hi = dmul(static_cast<double>(te), P.Q.tau);
+                lo = (a_lo < P.cam.near_plane) ? P.cam.near_plane : a_lo;
+                const double hi = (P.cam.far_plane < a_hi) ? P.cam.far_plane : a_hi;
+                if (hi > lo) {
+                    const double c = ceil(ddiv(dsub(hi, lo), P.step));
+                    n = c > 2.0 ? static_cast<int>(c) : 2;
+                    dt = ddiv(dsub(hi, lo), static_cast<double>(n));
+                    if (P.tf0_clear) {
+                        bool zero = true;
+#pragma unroll
+                        for (int d = 0; d <= D; ++d) zero &= w.pool[d * P.cap + slot] == 0;
+                        if (zero) n = 0;  // alpha = 1 - exp(-0) = 0 exactly: no colour, T unchanged
+                    }
+                }
+            }
+            const int incl = warp_incl_scan(n, lane);
+            const int total = __shfl_sync(kFull, incl, 31);
+            for (int base = 0; base < total && !term; base += 32) {
+                const int k = base + lane;
+                const bool act = k < total;
+                int lo_l = 0, hi_l = 31;
+#pragma unroll
+                for (int it = 0; it < 5; ++it) {
+                    const int mid = (lo_l + hi_l) >> 1;
+                    const int v = __shfl_sync(kFull, incl, mid);
+                    if (v > k)
+                        hi_l = mid;
+                    else
+                        lo_l = mid + 1;
+                }
+                const int j = lo_l;
+                const int s = k - (__shfl_sync(kFull, incl, j) - __shfl_sync(kFull, n, j));
+                const double lo_j = __shfl_sync(kFull, lo, j);
+                const double dt_j = __shfl_sync(kFull, dt, j);
+                const int64_t ts_j = __shfl_sync(kFull, ts, j);
+                const int slot_j = __shfl_sync(kFull, slot, j);
+                double alpha = 0.0, r = 0.0, g = 0.0, b = 0.0;
+                if (act) {
+                    // midpoint sample + evaluate_piece (raycast.hpp:295-301, 370-371)
+                    const double t = dadd(lo_j, dmul(dadd(static_cast<double>(s), 0.5), dt_j));
+                    const double x = dsub(ddiv(t, P.Q.tau), static_cast<double>(ts_j));
+                    double acc = 0.0;
+#pragma unroll
+                    for (int d = D; d >= 0; --d)
+                        acc = dadd(dmul(acc, x), static_cast<double>(static_cast<int64_t>(
+                                                     w.pool[d * P.cap + slot_j])));
+                    const double v = dmul(acc, P.Q.sigma);
+                    double ab;
+                    tf_sample(P.tf, P.ntf, v, r, g, b, ab);
+                    alpha = dsub(1.0, exp(dmul(-ab, dt_j)));  // raycast.hpp:372
+                }
+                // front to back: T before sample k = T * prod_{i<k} (1 - alpha_i)
+                const double f = act ? dsub(1.0, alpha) : 1.0;
+                double pre = f;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double u = __shfl_up_sync(kFull, pre, o);
+                    if (lane >= o) pre *= u;
+                }
+                double excl = __shfl_up_sync(kFull, pre, 1);
+                if (lane == 0) excl = 1.0;
+                const double Tb = T * excl;
+                // early ray termination once T <= 1e-3 (raycast.hpp:363, 369)
+                const unsigned okm = __ballot_sync(kFull, act && Tb > 1e-3);
+                const unsigned actm = __ballot_sync(kFull, act);
+                const unsigned fail = actm & ~okm;
+                const int first_fail = fail ? __ffs(fail) - 1 : 32;
+                const bool inc = act && lane < first_fail;
+                const double ta = inc ? dmul(Tb, alpha) : 0.0;
+                Cr += warp_sum(inc ? dmul(ta, r) : 0.0);
+                Cg += warp_sum(inc ? dmul(ta, g) : 0.0);
+                Cb += warp_sum(inc ? dmul(ta, b) : 0.0);
+                const unsigned incm = __ballot_sync(kFull, inc);
+                if (incm) T = __shfl_sync(kFull, dmul(Tb, f), 31 - __clz(incm));
+                if (fail) term = true;
+            }
+        }
+        // composited start pieces are dead: their slots return to the pool
+        free_slots(have, slot);
+        open_t = last_t;
+        open_slot = last_slot;
+        has_open = true;
+    }
+
+    // Finalise every pending knot with t < F (all of them if all_): equal
+    // positions merge, the running polynomial is the prefix sum of the jumps
+    // Taylor-shifted to a common origin tref (exact modulo 2^64, so equal to
+    // RayAccumulator's Int128 result whenever that fits int64), and each
+    // distinct position becomes a FieldPiece.
+    __device__ void flush(int64_t F, bool all_) {
+        const int nf = all_ ? np : lower_bound64(w.pt, np, F);
+        if (nf == 0) return;
+        for (int c0 = 0; c0 < nf; c0 += 32) {
+            const int i = c0 + lane;
+            const bool valid = i < nf;
+            int64_t t = 0;
+            int s = 0;
+            bool last = false;
+            if (valid) {
+                t = w.pt[i];
+                s = w.ps[i];
+                last = (i == nf - 1) || (w.pt[i + 1] != t);
+            }
+            if (!has_ref) {
+                tref = __shfl_sync(kFull, t, 0);
+                has_ref = true;
+            }
+            uint64_t g[D + 1];
+#pragma unroll
+            for (int d = 0; d <= D; ++d) g[d] = valid ? w.pool[d * P.cap + s] : 0ull;
+            taylor_shift<D>(g, static_cast<uint64_t>(tref) - static_cast<uint64_t>(t));
+#pragma unroll
+            for (int d = 0; d <= D; ++d) {
+                g[d] = warp_incl_scan(g[d], lane) + G[d];
+                G[d] = __shfl_sync(kFull, g[d], 31);
+            }
+            const unsigned pm = __ballot_sync(kFull, last);
+            const int cp = __popc(pm);
+            if (last) {
+                taylor_shift<D>(g, static_cast<uint64_t>(t) - static_cast<uint64_t>(tref));
+#pragma unroll
+                for (int d = 0; d <= D; ++d) w.pool[d * P.cap + s] = g[d];
+                const int pr = __popc(pm & lanemask_lt());
+                w.nt[pr] = t;
+                w.ns[pr] = static_cast<uint16_t>(s);
+                if (P.dump_piece_t) {
+                    const unsigned long long at = atomicAdd(&P.dump_count[1], 1ull);
+                    if (at < P.dump_cap_pieces) {
+                        P.dump_piece_ray[at] = ray_id;
+                        P.dump_piece_t[at] = t;
+#pragma unroll
+                        for (int d = 0; d <= D; ++d)
+                            P.dump_piece_a[at * (D + 1) + d] = static_cast<int64_t>(g[d]);
+                    }
+                }
+            }
+            pieces += cp;
+            free_slots(valid && !last, s);
+            if (cp > 0) composite_chunk(cp);
+        }
+        // drop the flushed prefix
+        const int rest = np - nf;
+        for (int c0 = 0; c0 < rest; c0 += 32) {
+            const int i = c0 + lane;
+            int64_t t = 0;
+            uint16_t s = 0;
+            if (i < rest) {
+                t = w.pt[nf + i];
+                s = w.ps[nf + i];
+            }
+            __syncwarp();
+            if (i < rest) {
+                w.pt[i] = t;
+                w.ps[i] = s;
+            }
+            __syncwarp();
+        }
+        np = rest;
+    }
+
+    __device__ void report_overflow(int pi) {
+        const unsigned long long key = (static_cast<unsigned long long>(P.orig[pi]) << 32) | ray_id;
+        atomicMin(&P.stats[kStatOverflowKey], key);
+    }
+
+    // Quantize the first nq queued hits (lane per hit) and merge their knots
+    // into the sorted window.  Returns false if the window is too small.
+    __device__ bool insert_hits(int nq, int64_t F_pre) {
+        constexpr int R = C::R;
+        const bool act = lane < nq;
+        int pi = 0;
+        double lam = 0.0, tchi = 0.0, h = 0.0;
+        if (act) {
+            pi = w.hq_p[lane];
+            lam = w.hq_lam[lane];
+            tchi = w.hq_t[lane];
+            h = P.pxyzh[pi].w;
+        }
+        bool ovf = false;
+        HitPositions<M> hp;
+        bool emits = act && quantize_positions<M>(P.Q, h, lam, tchi, hp, ovf);
+        int nk = emits ? hp.nk : 0;
+        if (ovf) {
+            report_overflow(pi);
+            nk = 0;
+            emits = false;
+        }
+        const int off = warp_incl_scan(nk, lane) - nk;
+        const int total = __shfl_sync(kFull, off + nk, 31);
+        if (total == 0) return true;
+        if (total > nfree) {
+            flush(F_pre, false);
+            if (total > nfree) return false;
+        }
+        const int slot0 = nfree - total + off;  // this lane's slots: fl[slot0 .. slot0 + nk)
+        int64_t kt[R];
+        int ks[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            kt[r] = INT64_MAX;
+            ks[r] = 0;
+        }
+        if (emits) {
+            double X[2 * D];
+            const double* xs = P.xy + static_cast<size_t>(pi) * (2 * D);
+#pragma unroll
+            for (int d = 0; d < 2 * D; ++d) X[d] = xs[d];
+            quantize_emit<D, M>(P.Q, X, hp, ovf, [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
+                const int slot = w.fl[slot0 + o];
+#pragma unroll
+                for (int d = 0; d <= D; ++d) w.pool[d * P.cap + slot] = static_cast<uint64_t>(b[d]);
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    if (r == o) {
+                        kt[r] = t;
+                        ks[r] = slot;
+                    }
+            });
+            if (ovf) report_overflow(pi);
+        }
+        __syncwarp();
+        nfree -= total;
+
+        // sort the new knots, then merge them into the window in place:
+        // pending elements move up (highest chunk first), new ones fill the gaps
+        bitonic_sort<R>(kt, ks, lane);
+        int dB[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = lane * R + r;
+            dB[r] = 0;
+            if (e < total) {
+                w.nt[e] = kt[r];
+                w.ns[e] = static_cast<uint16_t>(ks[r]);
+                dB[r] = e + upper_bound64(w.pt, np, kt[r]);
+            }
+        }
+        __syncwarp();
+        for (int c0 = ((np - 1) / 32) * 32; np > 0 && c0 >= 0; c0 -= 32) {
+            const int i = c0 + lane;
+            int64_t t = 0;
+            uint16_t s = 0;
+            int dest = 0;
+            if (i < np) {
+                t = w.pt[i];
+                s = w.ps[i];
+                dest = i + lower_bound64(w.nt, total, t);
+            }
+            __syncwarp();
+            if (i < np) {
+                w.pt[dest] = t;
+                w.ps[dest] = s;
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = lane * R + r;
+            if (e < total) {
+                w.pt[dB[r]] = kt[r];
+                w.ps[dB[r]] = static_cast<uint16_t>(ks[r]);
+            }
+        }
+        __syncwarp();
+        np += total;
+        knots += total;
+        if (np > max_pending) max_pending = np;
+        return true;
+    }
+
+    // One ray; returns false if the knot window overflowed (ray is retried).
+    __device__ bool run(int px, int py) {
+        reset();
+        const RayD ray = make_ray(P.cam, px, py);
+        const int tile = (py >> kTileShift) * P.tiles_x + (px >> kTileShift);
+        const int local = P.nranks > 1 ? tile / P.nranks : tile;
+        const uint32_t cb = P.tile_begin[local], ce = P.tile_end[local];
+        const double near_plane = P.cam.near_plane, far_plane = P.cam.far_plane;
+        uint32_t cursor = cb;
+        int hq_n = 0;
+        while (true) {
+            // ---- gather: exact hit test of 32 candidates at a time
+            while (hq_n < 32 && cursor < ce) {
+                const uint32_t c = cursor + lane;
+                bool hit = false;
+                double lam = 0.0, tchi = 0.0;
+                uint32_t pi = 0;
+                if (c < ce) {
+                    pi = P.cand[c];
+                    const int4 bb = P.bbox[pi];
+                    if (px >= bb.x && px <= bb.y && py >= bb.z && py <= bb.w) {
+                        const double4 p = P.pxyzh[pi];
+                        hit = hit_ray(ray, p.x, p.y, p.z, dmul(P.Q.q, p.w), p.w, near_plane,
+                                      far_plane, lam, tchi);
+                    }
+                }
+                const unsigned m = __ballot_sync(kFull, hit);
+                if (hit) {
+                    const int at = hq_n + __popc(m & lanemask_lt());
+                    w.hq_c[at] = static_cast<int32_t>(c);
+                    w.hq_p[at] = static_cast<int32_t>(pi);
+                    w.hq_lam[at] = lam;
+                    w.hq_t[at] = tchi;
+                }
+                if (P.dump_hit_ray && m) {
+                    unsigned long long base = 0;
+                    if (lane == 0)
+                        base = atomicAdd(&P.dump_count[0], static_cast<unsigned long long>(__popc(m)));
+                    base = __shfl_sync(kFull, base, 0);
+                    if (hit) {
+                        const unsigned long long at = base + __popc(m & lanemask_lt());
+                        if (at < P.dump_cap_hits) {
+                            P.dump_hit_ray[at] = ray_id;
+                            P.dump_hit_pidx[at] = P.orig[pi];
+                            P.dump_hit_lam[at] = lam;
+                            P.dump_hit_tchi[at] = tchi;
+                        }
+                    }
+                }
+                hq_n += __popc(m);
+                hits += __popc(m);
+                cursor += 32;
+            }
+            __syncwarp();
+            if (hq_n > 0) {
+                const int nq = hq_n < 32 ? hq_n : 32;
+                const int64_t F_pre = knot_floor(P.front[P.cand[w.hq_c[0]]], P.Q.tau);
+                if (!insert_hits(nq, F_pre)) return false;
+                const int rest = hq_n - nq;
+                int32_t qc = 0, qp = 0;
+                double ql = 0.0, qt = 0.0;
+                if (lane < rest) {
+                    qc = w.hq_c[nq + lane];
+                    qp = w.hq_p[nq + lane];
+                    ql = w.hq_lam[nq + lane];
+                    qt = w.hq_t[nq + lane];
+                }
+                __syncwarp();
+                if (lane < rest) {
+                    w.hq_c[lane] = qc;
+                    w.hq_p[lane] = qp;
+                    w.hq_lam[lane] = ql;
+                    w.hq_t[lane] = qt;
+                }
+                __syncwarp();
+                hq_n = rest;
+            }
+            if (hq_n == 0 && cursor >= ce) {
+                flush(0, true);
+                break;
+            }
+            const uint32_t next = hq_n > 0 ? static_cast<uint32_t>(w.hq_c[0]) : cursor;
+            const int64_t F = knot_floor(P.front[P.cand[next]], P.Q.tau);
+            const int nf = lower_bound64(w.pt, np, F);
+            if (nf >= 32 || nfree < 32 * C::KN) flush(F, false);
+            if (term && P.mode == SPHRAY_MODE_FAST) break;
+        }
+        return true;
+    }
+
+    __device__ void finish(double* out) {
+        if (lane == 0) {
+            double r = P.bg[0], g = P.bg[1], b = P.bg[2];
+            if (knots > 0) {
+                // pixel = C + (1 - a) * background, a = 1 - T (raycast.hpp:379, 486-488)
+                const double a = 1.0 - T;
+                r = Cr + (1.0 - a) * P.bg[0];
+                g = Cg + (1.0 - a) * P.bg[1];
+                b = Cb + (1.0 - a) * P.bg[2];
+            }
+            out[0] = r;
+            out[1] = g;
+            out[2] = b;
+            const bool complete = !(term && P.mode == SPHRAY_MODE_FAST);
+            bool residual = false;  // raycast.hpp:477-480: trailing piece must be zero
+            if (knots > 0 && complete && has_open) {
+#pragma unroll
+                for (int d = 0; d <= D; ++d) residual |= w.pool[d * P.cap + open_slot] != 0;
+            }
+            // RayAccumulator op count for P distinct positions (raycast.hpp:217-244)
+            const unsigned long long Pp = pieces;
+            const unsigned long long ops =
+                Pp > 0 ? Pp * (D + 1) + (Pp - 1) * ((D + 1) * (3 * D + 4) / 2) : 0ull;
+            if (knots) {
+                atomicAdd(&P.stats[kStatKnots], knots);
+                atomicAdd(&P.stats[kStatRays], 1ull);
+                atomicAdd(&P.stats[kStatIntOps], ops);
+                if (residual) atomicAdd(&P.stats[kStatResidual], 1ull);
+            }
+            if (hits) atomicAdd(&P.stats[kStatHits], hits);
+            atomicMax(&P.stats[kStatMaxPending], static_cast<unsigned long long>(max_pending));
+        }
+        __syncwarp();
+    }
+};
+
+template <int D, int M>
+__global__ void __launch_bounds__(256) k_render_rays(const FrameParams P) {
+    extern __shared__ __align__(16) char smem[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const WarpMem wm = carve(smem + static_cast<size_t>(warp) * P.warp_bytes, D, P.cap, Cfg<M>::NB);
+    RayWorker<D, M> rw(P, wm, lane);
+    while (true) {
+        unsigned long long item = 0;
+        if (lane == 0) item = atomicAdd(P.work_counter, 1ull);
+        item = __shfl_sync(kFull, item, 0);
+        if (item >= P.total_work) break;
+        int px, py;
+        if (P.ray_list) {
+            const uint32_t rid = P.ray_list[item];
+            px = static_cast<int>(rid % static_cast<uint32_t>(P.cam.W));
+            py = static_cast<int>(rid / static_cast<uint32_t>(P.cam.W));
+        } else {
+            const uint64_t local = item / kTileRays;
+            const int r = static_cast<int>(item % kTileRays);
+            const uint64_t tile = P.nranks > 1 ? local * P.nranks + P.rank : local;
+            const int tx = static_cast<int>(tile % P.tiles_x), ty = static_cast<int>(tile / P.tiles_x);
+            px = tx * kTile + (r & (kTile - 1));
+            py = ty * kTile + (r >> kTileShift);
+        }
+        if (px >= P.cam.W || py >= P.cam.H) continue;
+        rw.ray_id = static_cast<uint64_t>(py) * P.cam.W + px;
+        uint64_t out_index = rw.ray_id;
+        if (P.packed) {
+            const uint64_t tile = static_cast<uint64_t>(py >> kTileShift) * P.tiles_x + (px >> kTileShift);
+            out_index = (tile / P.nranks) * kTileRays + ((py & (kTile - 1)) << kTileShift) + (px & (kTile - 1));
+        }
+        if (rw.run(px, py)) {
+            rw.finish(P.rgb + out_index * 3);
+        } else if (lane == 0) {
+            const unsigned at = atomicAdd(P.retry_count, 1u);
+            P.retry_list[at] = static_cast<uint32_t>(rw.ray_id);
+        }
+        __syncwarp();
+    }
+}
+
+// quantize_particle for explicit hits (validation entry point).
+template <int D, int M>
+__global__ void k_quantize_hits(const QuantParams Q, const sphray_particle* ps, const double* powh,
+                                const double* powtau, size_t nhits, const double* tchi,
+                                const double* lam, int64_t* knot_t, int64_t* knot_b,
+                                int32_t* knot_count) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nhits) return;
+    constexpr int KN = 2 * M + 1;
+    const sphray_particle p = ps[i];
+    bool ovf = false;
+    HitPositions<M> hp;
+    if (!quantize_positions<M>(Q, p.h, lam[i], tchi[i], hp, ovf)) {
+        knot_count[i] = ovf ? -1 : 0;
+        return;
+    }
+    double X[2 * D];
+    for (int d = 1; d <= D; ++d) {
+        X[d - 1] = dmul(dmul(powtau[d - 1], p.mass), p.value);
+        X[D + d - 1] = dmul(dmul(Q.sigma, p.density), powh[i * D + d - 1]);
+    }
+    const int stride = Q.K + 1;
+    quantize_emit<D, M>(Q, X, hp, ovf, [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
+        if (o < KN && o < stride) {
+            knot_t[i * stride + o] = t;
+            for (int d = 0; d <= D; ++d) knot_b[(i * stride + o) * (D + 1) + d] = b[d];
+        }
+    });
+    knot_count[i] = ovf ? -1 : hp.nk;
+}
+
+
+}  // namespace rk
+
+#define SPHRAY_RK_CUDA_OK(x)                                                       \
+    do {                                                                           \
+        cudaError_t e_ = (x);                                                      \
+        if (e_ != cudaSuccess)                                                     \
+            fail(SPHRAY_ERR_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <int D, int M>
+int render_occupancy_t(int warps, size_t smem) {
+    int nb = 0;
+    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(rk::k_render_rays<D, M>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem)));
+    SPHRAY_RK_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, rk::k_render_rays<D, M>,
+                                                                    warps * 32, smem));
+    return nb;
+}
+
+template <int D, int M>
+void launch_render_t(const FrameParams& P, int blocks, int warps, cudaStream_t s) {
+    const size_t smem = static_cast<size_t>(P.warp_bytes) * warps;
+    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(rk::k_render_rays<D, M>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem)));
+    rk::k_render_rays<D, M><<<blocks, warps * 32, smem, s>>>(P);
+    SPHRAY_RK_CUDA_OK(cudaGetLastError());
+}
+
+template <int D, int M>
+void launch_quantize_hits_t(const QuantParams& Q, const sphray_particle* ps, const double* powh,
+                            const double* powtau, size_t nhits, const double* tchi,
+                            const double* lam, int64_t* knot_t, int64_t* knot_b,
+                            int32_t* knot_count, cudaStream_t s) {
+    rk::k_quantize_hits<D, M><<<static_cast<unsigned>((nhits + 127) / 128), 128, 0, s>>>(
+        Q, ps, powh, powtau, nhits, tchi, lam, knot_t, knot_b, knot_count);
+    SPHRAY_RK_CUDA_OK(cudaGetLastError());
+}
+
+#define SPHRAY_INSTANTIATE(D, M)                                                             \
+    template int render_occupancy_t<D, M>(int, size_t);                                      \
+    template void launch_render_t<D, M>(const FrameParams&, int, int, cudaStream_t);         \
+    template void launch_quantize_hits_t<D, M>(const QuantParams&, const sphray_particle*,   \
+                                               const double*, const double*, size_t,         \
+                                               const double*, const double*, int64_t*,       \
+                                               int64_t*, int32_t*, cudaStream_t);
+
+}  // namespace sphray_b200

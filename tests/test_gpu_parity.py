@@ -1,0 +1,258 @@
+"""GPU parity: the sm_100a path against the reference on identical inputs.
+
+Checkers: the golden fixtures of tests/golden/ (produced by the UNMODIFIED
+reference through oracle/_ref by tests/golden/make_golden.py) and, for
+generated scenes, oracle/_ref run live on the GPU box's host.
+
+Bars:
+  * hit sets (ray, particle, lam, t_chi): bit-exact
+  * per-hit knots and merged FieldPiece coefficients: bit-exact integers
+    (reference accumulate<Int128> on w64 quanta, identical to the int64 path
+    whenever that does not throw: raycast_tests.cpp:440-442)
+  * RGB: |gpu - reference| <= 1e-4 absolute per channel.  Both compute in
+    fp64; the residual differences are CUDA-vs-glibc exp ulps and the order of
+    the front-to-back sum (observed ~1e-15).
+  * RenderStats particles / skipped / knots / rays_touched / int_ops /
+    residual_failures / step: exact (EXACT mode)
+"""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import paper_2401_02896_b200 as S
+from oracle import ref
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+RGB_TOL = 1e-4
+GOLDEN_SCENES = ["render_test", "footprint_ortho", "footprint_pinhole", "clip_planes", "desk",
+                 "blob3000", "kd_K3_D2", "kd_K5_D4", "kd_K2_D3", "kd_K6_D6", "kd_K7_D5"]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = S.Context(0)
+    yield c
+    c.close()
+
+
+def load(name):
+    z = np.load(os.path.join(H.GOLDEN, name + ".npz"))
+    g = {k: z[k] for k in z.files}
+    ck = dict(mode=str(g["cam_mode"]), position=tuple(g["cam_position"]),
+              look_at=tuple(g["cam_look_at"]), up=tuple(g["cam_up"]), width=int(g["cam_width"]),
+              height=int(g["cam_height"]), fov_deg=float(g["cam_fov_deg"]),
+              ortho_height=float(g["cam_ortho_height"]), near=float(g["cam_near"]),
+              far=float(g["cam_far"]))
+    g["ck"] = ck
+    g["lut_path"] = os.path.join(H.LUTS, str(g["lut"]))
+    return g
+
+
+def digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def quanta(g):
+    return S.QuantaConfig(float(g["tau"]), float(g["sigma"]), 64)
+
+
+def dstats(g, ps, lut):
+    return S.dataset_stats(ps, lut)
+
+
+@pytest.mark.parametrize("name", GOLDEN_SCENES)
+def test_hit_sets_bit_exact(ctx, name):
+    g = load(name)
+    lut = S.load_lut(g["lut_path"])
+    ctx.upload(g["particles"], lut)
+    ray, pid, lam, t = ctx.hits(S.Camera(**g["ck"]))
+    if "digest_hits" in g:
+        # reference order is particle-major; compare in the same order
+        o = np.lexsort((ray, pid))
+        assert len(ray) == int(g["n_hits"])
+        assert digest(ray[o], pid[o], lam[o], t[o]) == str(g["digest_hits"])
+        return
+    o = np.lexsort((g["hit_pidx"], g["hit_ray"]))
+    np.testing.assert_array_equal(ray, g["hit_ray"][o])
+    np.testing.assert_array_equal(pid, g["hit_pidx"][o])
+    np.testing.assert_array_equal(lam.view(np.uint64), g["hit_lam"][o].view(np.uint64))
+    np.testing.assert_array_equal(t.view(np.uint64), g["hit_tchi"][o].view(np.uint64))
+
+
+@pytest.mark.parametrize("name", [n for n in GOLDEN_SCENES if n not in ("desk", "blob3000")])
+def test_knots_bit_exact(ctx, name):
+    g = load(name)
+    lut = S.load_lut(g["lut_path"])
+    ps = g["particles"]
+    kt, kb, kc = ctx.quantize_hits(ps[g["hit_pidx"]], g["hit_tchi"], g["hit_lam"], lut, quanta(g))
+    np.testing.assert_array_equal(kc, g["knot_count"])
+    off = np.concatenate([[0], np.cumsum(g["knot_count"])])
+    D1 = lut.D + 1
+    for i in range(len(kc)):
+        np.testing.assert_array_equal(kt[i, : kc[i]], g["knot_t"][off[i]:off[i + 1]])
+        np.testing.assert_array_equal(kb[i, : kc[i]], g["knot_b"][off[i]:off[i + 1], :D1])
+
+
+@pytest.mark.parametrize("name", GOLDEN_SCENES)
+def test_field_pieces_bit_exact(ctx, name):
+    g = load(name)
+    lut = S.load_lut(g["lut_path"])
+    ctx.upload(g["particles"], lut)
+    p = ctx.pieces(S.Camera(**g["ck"]), quanta(g))
+    np.testing.assert_array_equal(p["rays"], g["pl_rays"])
+    np.testing.assert_array_equal(p["piece_off"], g["pl_piece_off"])
+    if "digest_pieces" in g:
+        assert len(p["piece_t"]) == int(g["n_pieces"])
+        # the reference stores 7 coefficients (max_degree + 1) per piece
+        pa = np.zeros((len(p["piece_a"]), lut.D + 1), np.int64)
+        pa[:] = p["piece_a"]
+        assert digest(p["rays"], p["piece_off"], p["piece_t"], pa) == str(g["digest_pieces"])
+        return
+    assert g["pl_piece_fits"].all()
+    np.testing.assert_array_equal(p["piece_t"], g["pl_piece_t"])
+    np.testing.assert_array_equal(p["piece_a"], g["pl_piece_a"])
+
+
+@pytest.mark.parametrize("name", GOLDEN_SCENES)
+@pytest.mark.parametrize("mode", [S.MODE_EXACT, S.MODE_FAST])
+def test_render_matches_reference(ctx, name, mode):
+    g = load(name)
+    lut = S.load_lut(g["lut_path"])
+    ps = g["particles"]
+    ds = S.dataset_stats(ps, lut)
+    assert ds.h_r == float(g["h_r"]) and ds.a_max == float(g["a_max"])
+    qc = S.choose_quanta(lut, ds)
+    assert qc.tau == float(g["tau"]) and qc.sigma == float(g["sigma"])
+    img, st = S.render_scene(ps, S.Camera(**g["ck"]), S.TransferFunction.from_array(g["tf"]), lut,
+                             qc, ds, S.RenderOptions(background=tuple(g["background"]), mode=mode),
+                             ctx=ctx)
+    err = np.abs(img.pixels - g["rgb"]).max()
+    assert err <= RGB_TOL, err
+    assert st.particles == int(g["stat_particles"])
+    assert st.skipped_particles == int(g["stat_skipped_particles"])
+    assert st.step == float(g["stat_step"])
+    if mode == S.MODE_EXACT:
+        for k in ("knots", "rays_touched", "int_ops", "residual_failures"):
+            assert getattr(st, k) == int(g["stat_" + k]), (k, getattr(st, k), int(g["stat_" + k]))
+
+
+def _blob(n, w):
+    ps = S.generate_scene(1, n=n)
+    return ps, H.synth_camera_kwargs(w, w)
+
+
+def test_generated_blob_against_live_reference(ctx):
+    """A generated config-1-family scene, checked against oracle/_ref on this host."""
+    ps, ck = _blob(20000, 96)
+    lut = S.load_lut(H.lut_path(4, 3, 1024))
+    rl = ref.Lut(H.lut_path(4, 3, 1024))
+    ds = S.dataset_stats(ps, lut)
+    qc = S.choose_quanta(lut, ds)
+    rqc = ref.RpQuanta(qc.tau, qc.sigma, 64)
+    rds = ref.dataset_stats(ps, rl)
+    ctx.upload(ps, lut)
+    ray, pid, lam, t = ctx.hits(S.Camera(**ck))
+    r_ray, r_pid, r_lam, r_t = ref.footprint(ps, ref.Camera(**ck), lut.q)
+    o = np.lexsort((r_pid, r_ray))
+    np.testing.assert_array_equal(ray, r_ray[o])
+    np.testing.assert_array_equal(pid, r_pid[o])
+    np.testing.assert_array_equal(lam.view(np.uint64), r_lam[o].view(np.uint64))
+    np.testing.assert_array_equal(t.view(np.uint64), r_t[o].view(np.uint64))
+    p = ctx.pieces(S.Camera(**ck), qc)
+    r = ref.pipeline(ps, ref.Camera(**ck), rl, rqc)
+    np.testing.assert_array_equal(p["rays"], r["rays"])
+    np.testing.assert_array_equal(p["piece_t"], r["piece_t"])
+    np.testing.assert_array_equal(p["piece_a"], r["piece_a"])
+    img, st = S.render_scene(ps, S.Camera(**ck), S.TransferFunction.from_array(H.SYNTH_TF), lut, qc,
+                             ds, ctx=ctx)
+    rgb, rst, _, _ = ref.render_robust(ps, ref.Camera(**ck), H.SYNTH_TF, rl, rqc, rds)
+    assert np.abs(img.pixels - rgb).max() <= RGB_TOL
+    for k in ("knots", "rays_touched", "int_ops", "residual_failures", "skipped_particles"):
+        assert getattr(st, k) == rst[k], k
+
+
+def test_early_termination_opaque(ctx):
+    """Opaque media saturate and exit early (raycast_tests.cpp:382-387)."""
+    g = load("blob3000")
+    lut = S.load_lut(g["lut_path"])
+    rl = ref.Lut(g["lut_path"])
+    ps = g["particles"]
+    ds = S.dataset_stats(ps, lut)
+    qc = S.choose_quanta(lut, ds)
+    rds = ref.dataset_stats(ps, rl)
+    dense = np.array([[0.0, 1.0, 0.5, 0.25, 0.0], [0.01, 1.0, 0.5, 0.25, 500.0]])
+    rgb, rst, _, _ = ref.render_robust(ps, ref.Camera(**g["ck"]), dense, rl,
+                                       ref.RpQuanta(qc.tau, qc.sigma, 64), rds)
+    assert (rgb.sum(axis=2) > 0.5).any()
+    for mode in (S.MODE_EXACT, S.MODE_FAST):
+        img, st = S.render_scene(ps, S.Camera(**g["ck"]), S.TransferFunction.from_array(dense), lut,
+                                 qc, ds, S.RenderOptions(mode=mode), ctx=ctx)
+        assert np.abs(img.pixels - rgb).max() <= RGB_TOL
+        if mode == S.MODE_EXACT:
+            assert st.knots == rst["knots"] and st.int_ops == rst["int_ops"]
+
+
+def test_empty_scene_paints_background(ctx):
+    """raycast_tests.cpp:445-470."""
+    lut = S.load_lut(H.lut_path(4, 3, 16))
+    cam = S.Camera(width=6, height=4)
+    img, st = S.render_scene(np.zeros((0, 7)), cam, S.TransferFunction.from_array([[0, 0, 0, 0, 0.5]]),
+                             lut, S.QuantaConfig(0.1, 1.0, 64), S.DatasetStats(h_r=1.0),
+                             S.RenderOptions(background=(0.25, 0.5, 0.75)), ctx=ctx)
+    assert st.particles == 0 and st.knots == 0 and st.rays_touched == 0
+    assert (img.pixels == np.array([0.25, 0.5, 0.75])).all()
+
+
+def test_permutation_invariance(ctx):
+    """raycast_tests.cpp:422-432: permuting the input changes no bit."""
+    g = load("render_test")
+    lut = S.load_lut(g["lut_path"])
+    ps = g["particles"]
+    ds = S.dataset_stats(ps, lut)
+    qc = S.choose_quanta(lut, ds)
+    args = (S.Camera(**g["ck"]), S.TransferFunction.from_array(g["tf"]), lut, qc, ds,
+            S.RenderOptions(background=tuple(g["background"])))
+    img, st = S.render_scene(ps, *args, ctx=ctx)
+    for seed in (1, 2, 3):
+        p2 = ps[np.random.default_rng(seed).permutation(len(ps))]
+        img2, st2 = S.render_scene(p2, *args, ctx=ctx)
+        assert (img2.pixels == img.pixels).all()
+        assert st2.knots == st.knots and st2.residual_failures == 0
+
+
+def test_small_window_retry_is_exact(ctx):
+    """A tiny knot window forces the wide-window retry pass; results must not change."""
+    ps, ck = _blob(20000, 64)
+    lut = S.load_lut(H.lut_path(4, 3, 1024))
+    ds = S.dataset_stats(ps, lut)
+    qc = S.choose_quanta(lut, ds)
+    cam, tf = S.Camera(**ck), S.TransferFunction.from_array(H.SYNTH_TF)
+    img, st = S.render_scene(ps, cam, tf, lut, qc, ds, S.RenderOptions(), ctx=ctx)
+    img2, st2 = S.render_scene(ps, cam, tf, lut, qc, ds, S.RenderOptions(window=192), ctx=ctx)
+    assert st2.window_retries > 0
+    # exact integers; only the fp64 association of the compositing sum follows
+    # the window's flush points
+    assert np.abs(img2.pixels - img.pixels).max() <= 1e-12
+    assert st2.knots == st.knots and st2.int_ops == st.int_ops
+
+
+def test_validation_errors(ctx):
+    lut = S.load_lut(H.lut_path(4, 3, 16))
+    ps = H.random_cloud(H.MT19937_64(1), 10, 1.0, -1.0, 1.0)
+    tf = S.TransferFunction.from_array([[0, 0, 0, 0, 0.5]])
+    q, d = S.QuantaConfig(0.1, 1.0), S.DatasetStats(h_r=1.0)
+    with pytest.raises(S.ConfigError):
+        S.render_scene(ps, S.Camera(width=0), tf, lut, q, d, ctx=ctx)
+    with pytest.raises(S.ConfigError):
+        S.render_scene(ps, S.Camera(), S.TransferFunction.from_array([[1, 0, 0, 0, 0], [1, 0, 0, 0, 0]]),
+                       lut, q, d, ctx=ctx)
+    with pytest.raises(S.ConfigError):
+        S.render_scene(ps, S.Camera(), S.TransferFunction.from_array([[0, 0, 0, 0, -1.0]]), lut, q, d,
+                       ctx=ctx)
