@@ -121,7 +121,10 @@ typedef struct sphray_render_stats {
     uint64_t candidates;      /* binned (tile, particle) entries */
     uint64_t window_retries;  /* rays re-run with a wider knot window */
     uint64_t max_window;      /* largest pending-knot count seen */
-    double device_ms;         /* device time of the render (CUDA events) */
+    double device_ms;         /* device time of the whole frame (CUDA events) */
+    double bin_ms;            /* particle prep + tile binning (sort) */
+    double render_ms;         /* the render kernel(s): gather, quantize, merge, composite */
+    uint64_t launches;        /* kernels launched for the frame (ours + CUB's) */
 } sphray_render_stats;
 
 /* OverflowError carries particle index and ray id (errors.hpp:54-63). */
@@ -185,6 +188,10 @@ sphray_status sphray_scene_render(sphray_context* ctx, const sphray_camera* cam,
                                   const sphray_render_options* opts, double* rgb_out,
                                   sphray_render_stats* out_stats, sphray_error* err);
 const double* sphray_scene_device_image(sphray_context* ctx);
+
+/* The context's CUDA stream (cudaStream_t), for callers that time or order
+ * work around the library's launches. */
+void* sphray_context_stream(sphray_context* ctx);
 
 /* -------------------------------------------------------------------------
  * Validation outputs (the reference's cmd_validate harness, sphray_main.cpp:

@@ -127,7 +127,9 @@ class _RStats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("particles", "skipped_particles", "knots",
                                            "rays_touched", "int_ops", "residual_failures")] + [
         ("step", C.c_double)] + [(n, C.c_uint64) for n in (
-            "hits", "candidates", "window_retries", "max_window")] + [("device_ms", C.c_double)]
+            "hits", "candidates", "window_retries", "max_window")] + [
+        ("device_ms", C.c_double), ("bin_ms", C.c_double), ("render_ms", C.c_double),
+        ("launches", C.c_uint64)]
 
 
 class _Error(C.Structure):
@@ -170,6 +172,8 @@ def load_library():
                                       P(_RStats), P(_Error)]
     L.sphray_scene_device_image.argtypes = [C.c_void_p]
     L.sphray_scene_device_image.restype = C.c_void_p
+    L.sphray_context_stream.argtypes = [C.c_void_p]
+    L.sphray_context_stream.restype = C.c_void_p
     L.sphray_scene_hits.argtypes = [C.c_void_p, P(_Camera), P(C.c_uint64), P(C.c_int64),
                                     P(C.c_double), P(C.c_double), C.c_size_t, P(C.c_size_t),
                                     P(_Error)]
@@ -332,6 +336,9 @@ class RenderStats:
     window_retries: int = 0
     max_window: int = 0
     device_ms: float = 0.0
+    bin_ms: float = 0.0
+    render_ms: float = 0.0
+    launches: int = 0
 
     @classmethod
     def _from(cls, s: _RStats) -> "RenderStats":
@@ -505,6 +512,10 @@ class Context:
             C.byref(err)), err)
         img = Image(cam.width, cam.height, rgb) if to_host else None
         return img, RenderStats._from(rs)
+
+    def stream_ptr(self) -> int:
+        """The library's cudaStream_t (for torch.cuda.ExternalStream / event timing)."""
+        return int(self._L.sphray_context_stream(self._h) or 0)
 
     def device_image_ptr(self) -> int:
         return int(self._L.sphray_scene_device_image(self._h) or 0)

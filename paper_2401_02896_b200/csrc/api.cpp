@@ -130,6 +130,11 @@ sphray_status sphray_scene_render(sphray_context* ctx, const sphray_camera* cam,
     });
 }
 
+void* sphray_context_stream(sphray_context* ctx) {
+    if (!ctx || !ctx->engine) return nullptr;
+    return ctx->engine->stream();
+}
+
 const double* sphray_scene_device_image(sphray_context* ctx) {
     if (!ctx || !ctx->engine) return nullptr;
     return ctx->engine->device_image();

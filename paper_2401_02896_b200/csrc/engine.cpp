@@ -114,13 +114,16 @@ Engine::Engine(int device) : device_(device) {
     CUDA_OK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     CUDA_OK(cudaEventCreate(&ev0_));
     CUDA_OK(cudaEventCreate(&ev1_));
+    CUDA_OK(cudaEventCreate(&evb_));
+    CUDA_OK(cudaEventCreate(&evr0_));
+    CUDA_OK(cudaEventCreate(&evr1_));
 }
 
 Engine::~Engine() {
     cudaSetDevice(device_);
     if (comm_ && nccl().ok) nccl().CommDestroy(static_cast<ncclComm_t>(comm_));
-    if (ev0_) cudaEventDestroy(ev0_);
-    if (ev1_) cudaEventDestroy(ev1_);
+    for (cudaEvent_t e : {ev0_, ev1_, evb_, evr0_, evr1_})
+        if (e) cudaEventDestroy(e);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -283,6 +286,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     CUDA_OK(cudaMemsetAsync(d_dump_count_.p, 0, 16, s));
 
     CUDA_OK(cudaEventRecord(ev0_, s));
+    uint64_t launches = 0;
     // ---- binning: reference bbox -> (tile, front) keys -> radix sort
     uint64_t entries = 0;
     if (n > 0) {
@@ -310,6 +314,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         pp.rank = rank_;
         pp.nranks = nranks_;
         launch_prep(pp, s);
+        launches += 1 + 2;  // k_prep + CUB scan (init + scan)
         const size_t scan_b = cub_scan_bytes(n);
         d_tmp_.ensure(scan_b);
         cub_scan(d_counts_.as<uint32_t>(), d_offsets_.as<uint32_t>(), n, d_tmp_.p, d_tmp_.bytes, s);
@@ -339,6 +344,8 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
                      d_tmp_.bytes, s);
             launch_tile_ranges(d_keys2_.as<unsigned long long>(), entries,
                                d_tile_begin_.as<uint32_t>(), d_tile_end_.as<uint32_t>(), s);
+            // k_emit + onesweep radix sort (histogram, exclusive sum, one pass per 8 bits) + ranges
+            launches += 1 + 2 + (end_bit + 7) / 8 + 1;
         }
     } else {
         d_tile_begin_.ensure(owned_max * 4);
@@ -436,7 +443,11 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     if (bps < 1) bps = 1;
     CUDA_OK(cudaMemsetAsync(d_work_.p, 0, 8, s));
     CUDA_OK(cudaMemsetAsync(d_retry_count_.p, 0, 8, s));
-    if (P.total_work > 0) launch_render(P, D, m, sm_count_ * bps, warps, s);
+    CUDA_OK(cudaEventRecord(evr0_, s));
+    if (P.total_work > 0) {
+        launch_render(P, D, m, sm_count_ * bps, warps, s);
+        ++launches;
+    }
 
     // ---- rays whose window overflowed: once more with the widest window
     unsigned retry = 0;
@@ -457,6 +468,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         int bps2 = max_blocks_per_sm(D, m, 1, P2.warp_bytes);
         if (bps2 < 1) bps2 = 1;
         launch_render(P2, D, m, std::min<int>(retry, sm_count_ * bps2), 1, s);
+        ++launches;
         unsigned retry2 = 0;
         CUDA_OK(cudaMemcpyAsync(&retry2, d_retry_count_.as<unsigned int>() + 1, 4,
                                 cudaMemcpyDeviceToHost, s));
@@ -465,10 +477,13 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
             fail(SPHRAY_ERR_CAPACITY, std::to_string(retry2) + " rays exceed the widest knot window (" +
                                           std::to_string(cap2) + " knots)");
     }
+    CUDA_OK(cudaEventRecord(evr1_, s));
     // skipped_particles: counted once (rank 0), the particle set is replicated
-    if (rank_ == 0)
+    if (rank_ == 0 && n > 0) {
         launch_reach(C, n, lut_.q, d_pxyzh_.as<double4>(), d_bbox_.as<int4>(),
                      d_stats_.as<unsigned long long>() + kStatSkipped, s);
+        ++launches;
+    }
 
     // ---- gather finished tiles over NCCL (image-tile sharding)
     unsigned long long st[kStatCount];
@@ -504,8 +519,10 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         CUDA_OK(cudaEventRecord(ev1_, s));
         CUDA_OK(cudaStreamSynchronize(s));
     }
-    float ms = 0.0f;
+    float ms = 0.0f, ms_bin = 0.0f, ms_render = 0.0f;
     CUDA_OK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    CUDA_OK(cudaEventElapsedTime(&ms_bin, ev0_, evr0_));
+    CUDA_OK(cudaEventElapsedTime(&ms_render, evr0_, evr1_));
 
     if (st[kStatOverflowKey] != ~0ull) {
         // quantize_particle's OverflowError names the particle and ray (quantize.hpp:244-249)
@@ -566,6 +583,9 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         o.window_retries = retry;
         o.max_window = st[kStatMaxPending];
         o.device_ms = ms;
+        o.bin_ms = ms_bin;
+        o.render_ms = ms_render;
+        o.launches = launches + (packed && comm_ ? 3 : 0);
         *out = o;
     }
 }

@@ -64,6 +64,7 @@ class Engine {
                        const double* lam, const sphray_lut_view& lut, const sphray_quanta& qc,
                        int64_t* knot_t, int64_t* knot_b, int32_t* knot_count);
     const double* device_image() const { return d_image_.as<double>(); }
+    void* stream() const { return stream_; }
     bool has_scene() const { return has_scene_; }
     int rank() const { return rank_; }
     int nranks() const { return nranks_; }
@@ -73,7 +74,7 @@ class Engine {
     int device_ = 0;
     int sm_count_ = 0;
     cudaStream_t stream_ = nullptr;
-    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, evb_ = nullptr, evr0_ = nullptr, evr1_ = nullptr;
     // communicator (tile gather)
     int rank_ = 0, nranks_ = 1;
     void* comm_ = nullptr;
