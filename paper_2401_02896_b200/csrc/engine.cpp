@@ -389,6 +389,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     P.tiles_y = tiles_y;
     P.rank = rank_;
     P.nranks = nranks_;
+    P.inv_tau = 1.0 / qc.tau;
     P.tf = d_tf_.as<double>();
     P.ntf = static_cast<int>(ntf);
     P.tf0_clear = tf_absorption_at_zero(tf, ntf) == 0.0;

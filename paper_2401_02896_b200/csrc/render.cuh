@@ -63,6 +63,7 @@ struct FrameParams {
     const uint32_t* tile_end;
     int tiles_x, tiles_y;
     int rank, nranks;
+    double inv_tau;  // 1 / tau for sample abscissae (compositing only)
     // transfer function (raycast.hpp:313-338)
     const double* tf;  // ntf * 5
     int ntf;

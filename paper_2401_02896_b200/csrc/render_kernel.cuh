@@ -103,49 +103,60 @@ __device__ __forceinline__ void tf_sample(const double* tf, int n, double v, dou
 
 // Warp bitonic sort of 32*R (t, slot) pairs held R per lane (blocked layout:
 // element e = lane*R + r).  Ascending in t; equal t may end in any order
-// (their jumps are summed).
+// (their jumps are summed).  The (size, stride) stage loop is
+// a runtime loop so the code stays small (the render kernel is instruction-
+// cache bound when this is fully unrolled); only the per-register bodies are
+// unrolled: one cross-lane body and one intra-lane body per stride < R.
+template <int R, int J>
+__device__ __forceinline__ void bitonic_intra(int64_t (&t)[R], int (&s)[R], int lane, int size) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if ((r & J) == 0) {
+            const int r2 = r | J;
+            const bool asc = (((lane * R) + r) & size) == 0;
+            const bool sw = asc ? (t[r] > t[r2]) : (t[r] < t[r2]);
+            const int64_t a = t[r], b = t[r2];
+            const int sa = s[r], sb = s[r2];
+            t[r] = sw ? b : a;
+            t[r2] = sw ? a : b;
+            s[r] = sw ? sb : sa;
+            s[r2] = sw ? sa : sb;
+        }
+    }
+}
+
 template <int R>
 __device__ __forceinline__ void bitonic_sort(int64_t (&t)[R], int (&s)[R], int lane) {
-#pragma unroll
+#pragma unroll 1
     for (int size = 2; size <= 32 * R; size <<= 1) {
+#pragma unroll 1
+        for (int stride = size >> 1; stride >= 1; stride >>= 1) {
+            if (stride >= R) {
+                const int ls = stride / R;
+                const bool asc = ((lane * R) & size) == 0;
+                const bool keep_min = ((lane & ls) == 0) == asc;
 #pragma unroll
-        for (int stride = size / 2; stride >= R; stride >>= 1) {
-            const int ls = stride / R;
-            const bool asc = ((lane * R) & size) == 0;
-            const bool lower = (lane & ls) == 0;
-            const bool keep_min = lower == asc;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int64_t ot = __shfl_xor_sync(kFull, t[r], ls);
-                const int os = __shfl_xor_sync(kFull, s[r], ls);
-                const bool take = keep_min ? (ot < t[r]) : (ot > t[r]);
-                if (take) {
-                    t[r] = ot;
-                    s[r] = os;
+                for (int r = 0; r < R; ++r) {
+                    const int64_t ot = __shfl_xor_sync(kFull, t[r], ls);
+                    const int os = __shfl_xor_sync(kFull, s[r], ls);
+                    const bool take = keep_min ? (ot < t[r]) : (ot > t[r]);
+                    t[r] = take ? ot : t[r];
+                    s[r] = take ? os : s[r];
                 }
-            }
-        }
-#pragma unroll
-        for (int stride = (size / 2 < R ? size / 2 : R / 2); stride >= 1; stride >>= 1) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                if ((r & stride) == 0) {
-                    const int r2 = r | stride;
-                    const bool asc = (((lane * R) + r) & size) == 0;
-                    const bool sw = asc ? (t[r] > t[r2]) : (t[r] < t[r2]);
-                    if (sw) {
-                        const int64_t tt = t[r];
-                        t[r] = t[r2];
-                        t[r2] = tt;
-                        const int ss = s[r];
-                        s[r] = s[r2];
-                        s[r2] = ss;
-                    }
-                }
+            } else if (stride == 8 && R > 8) {
+                bitonic_intra<R, (R > 8 ? 8 : 1)>(t, s, lane, size);
+            } else if (stride == 4) {
+                bitonic_intra<R, 4>(t, s, lane, size);
+            } else if (stride == 2) {
+                bitonic_intra<R, 2>(t, s, lane, size);
+            } else {
+                bitonic_intra<R, 1>(t, s, lane, size);
             }
         }
     }
 }
+
+constexpr int kLaneSamples = 8;  // pieces up to this many samples are sampled lane-locally
 
 template <int M>
 struct Cfg {
@@ -240,11 +251,43 @@ class RayWorker {
         __syncwarp();
     }
 
+    // Samples of one piece, front to back, from transmittance T0 (composite(),
+    // raycast.hpp:369-377): midpoint t = lo + (s + 0.5) dt exactly as the
+    // reference places them; the piece polynomial (evaluate_piece,
+    // raycast.hpp:295-301) in fp64 Horner; alpha = 1 - exp(-absorption dt)
+    // through fp32 expm1 (relative error ~1e-7, inside the stated 1e-4 RGB
+    // tolerance); colour and transmittance accumulate in fp64.  With `stop`
+    // the reference's T > 1e-3 check runs before every sample.
+    __device__ __forceinline__ void sample_piece(const double (&c)[D + 1], int64_t ts, double lo,
+                                                 double dt, int n, double T0, bool stop,
+                                                 double& T, double& cr, double& cg, double& cb) const {
+        T = T0;
+        cr = cg = cb = 0.0;
+        const double tsd = static_cast<double>(ts);
+        for (int s = 0; s < n; ++s) {
+            if (stop && !(T > 1e-3)) break;
+            const double t = dadd(lo, dmul(dadd(static_cast<double>(s), 0.5), dt));
+            const double x = t * P.inv_tau - tsd;
+            double acc = c[D];
+#pragma unroll
+            for (int d = D - 1; d >= 0; --d) acc = fma(acc, x, c[d]);
+            double r, g, b, ab;
+            tf_sample(P.tf, P.ntf, acc * P.Q.sigma, r, g, b, ab);
+            const double alpha = static_cast<double>(-expm1f(static_cast<float>(-ab * dt)));
+            const double ta = T * alpha;
+            cr = fma(ta, r, cr);
+            cg = fma(ta, g, cg);
+            cb = fma(ta, b, cb);
+            T = T * (1.0 - alpha);
+        }
+    }
+
     // Composite the pieces completed in this chunk: lane j (j < cp) takes the
     // piece that starts at the previous piece (the carried open piece for
-    // j == 0) and ends at staged piece j -- composite(), raycast.hpp:356-381,
-    // distributed over samples rather than pieces so long gaps do not
-    // serialise one lane.
+    // j == 0) and ends at staged piece j.  Each lane samples its own piece
+    // sequentially; one warp combine (prefix product of transmittances,
+    // weighted colour sum) then folds the chunk into the ray.  Pieces with
+    // many samples (long gaps) go through a sample-parallel path instead.
     __device__ void composite_chunk(int cp) {
         const bool have = lane < cp && (lane > 0 || has_open);
         int64_t ts = 0, te = 0;
@@ -265,6 +308,9 @@ class RayWorker {
         if (!term) {
             int n = 0;
             double lo = 0.0, dt = 0.0;
+            double c[D + 1];
+#pragma unroll
+            for (int d = 0; d <= D; ++d) c[d] = 0.0;
             if (have) {
                 // [lo, hi] = [t_i tau, t_{i+1} tau] cut to [near, far]   (raycast.hpp:364-368)
                 const double a_lo = dmul(static_cast<double>(ts), P.Q.tau);
@@ -272,56 +318,26 @@ class RayWorker {
                 lo = (a_lo < P.cam.near_plane) ? P.cam.near_plane : a_lo;
                 const double hi = (P.cam.far_plane < a_hi) ? P.cam.far_plane : a_hi;
                 if (hi > lo) {
-                    const double c = ceil(ddiv(dsub(hi, lo), P.step));
-                    n = c > 2.0 ? static_cast<int>(c) : 2;
+                    const double cc = ceil(ddiv(dsub(hi, lo), P.step));
+                    n = cc > 2.0 ? static_cast<int>(cc) : 2;
                     dt = ddiv(dsub(hi, lo), static_cast<double>(n));
-                    if (P.tf0_clear) {
-                        bool zero = true;
+                    bool zero = true;
 #pragma unroll
-                        for (int d = 0; d <= D; ++d) zero &= w.pool[d * P.cap + slot] == 0;
-                        if (zero) n = 0;  // alpha = 1 - exp(-0) = 0 exactly: no colour, T unchanged
+                    for (int d = 0; d <= D; ++d) {
+                        const int64_t a = static_cast<int64_t>(w.pool[d * P.cap + slot]);
+                        zero &= a == 0;
+                        c[d] = static_cast<double>(a);
                     }
+                    // alpha = 1 - exp(-0) = 0 exactly: no colour, T unchanged
+                    if (zero && P.tf0_clear) n = 0;
                 }
             }
-            const int incl = warp_incl_scan(n, lane);
-            const int total = __shfl_sync(kFull, incl, 31);
-            for (int base = 0; base < total && !term; base += 32) {
-                const int k = base + lane;
-                const bool act = k < total;
-                int lo_l = 0, hi_l = 31;
-#pragma unroll
-                for (int it = 0; it < 5; ++it) {
-                    const int mid = (lo_l + hi_l) >> 1;
-                    const int v = __shfl_sync(kFull, incl, mid);
-                    if (v > k)
-                        hi_l = mid;
-                    else
-                        lo_l = mid + 1;
-                }
-                const int j = lo_l;
-                const int s = k - (__shfl_sync(kFull, incl, j) - __shfl_sync(kFull, n, j));
-                const double lo_j = __shfl_sync(kFull, lo, j);
-                const double dt_j = __shfl_sync(kFull, dt, j);
-                const int64_t ts_j = __shfl_sync(kFull, ts, j);
-                const int slot_j = __shfl_sync(kFull, slot, j);
-                double alpha = 0.0, r = 0.0, g = 0.0, b = 0.0;
-                if (act) {
-                    // midpoint sample + evaluate_piece (raycast.hpp:295-301, 370-371)
-                    const double t = dadd(lo_j, dmul(dadd(static_cast<double>(s), 0.5), dt_j));
-                    const double x = dsub(ddiv(t, P.Q.tau), static_cast<double>(ts_j));
-                    double acc = 0.0;
-#pragma unroll
-                    for (int d = D; d >= 0; --d)
-                        acc = dadd(dmul(acc, x), static_cast<double>(static_cast<int64_t>(
-                                                     w.pool[d * P.cap + slot_j])));
-                    const double v = dmul(acc, P.Q.sigma);
-                    double ab;
-                    tf_sample(P.tf, P.ntf, v, r, g, b, ab);
-                    alpha = dsub(1.0, exp(dmul(-ab, dt_j)));  // raycast.hpp:372
-                }
-                // front to back: T before sample k = T * prod_{i<k} (1 - alpha_i)
-                const double f = act ? dsub(1.0, alpha) : 1.0;
-                double pre = f;
+            const int maxn = __reduce_max_sync(kFull, n);
+            if (maxn > 0 && maxn <= kLaneSamples) {
+                double Tl, cr, cg, cb;
+                sample_piece(c, ts, lo, dt, n, 1.0, false, Tl, cr, cg, cb);
+                // exclusive prefix product of the lanes' transmittances
+                double pre = Tl;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const double u = __shfl_up_sync(kFull, pre, o);
@@ -329,20 +345,32 @@ class RayWorker {
                 }
                 double excl = __shfl_up_sync(kFull, pre, 1);
                 if (lane == 0) excl = 1.0;
-                const double Tb = T * excl;
-                // early ray termination once T <= 1e-3 (raycast.hpp:363, 369)
-                const unsigned okm = __ballot_sync(kFull, act && Tb > 1e-3);
-                const unsigned actm = __ballot_sync(kFull, act);
-                const unsigned fail = actm & ~okm;
-                const int first_fail = fail ? __ffs(fail) - 1 : 32;
-                const bool inc = act && lane < first_fail;
-                const double ta = inc ? dmul(Tb, alpha) : 0.0;
-                Cr += warp_sum(inc ? dmul(ta, r) : 0.0);
-                Cg += warp_sum(inc ? dmul(ta, g) : 0.0);
-                Cb += warp_sum(inc ? dmul(ta, b) : 0.0);
-                const unsigned incm = __ballot_sync(kFull, inc);
-                if (incm) T = __shfl_sync(kFull, dmul(Tb, f), 31 - __clz(incm));
-                if (fail) term = true;
+                const double Tb = T * excl;  // T before this lane's piece
+                const double Ta = Tb * Tl;   // T after it
+                // early ray termination (raycast.hpp:363, 369): the first piece
+                // that brings T to <= 1e-3 is replayed sample by sample
+                const unsigned failm = __ballot_sync(kFull, n > 0 && !(Ta > 1e-3));
+                const int f = failm ? __ffs(failm) - 1 : 32;
+                const bool inc = lane < f;
+                double rr = inc ? Tb * cr : 0.0, gg = inc ? Tb * cg : 0.0, bb = inc ? Tb * cb : 0.0;
+                double Tend = __shfl_sync(kFull, Ta, 31);
+                if (f < 32) {
+                    double Tr = 0.0, r2 = 0.0, g2 = 0.0, b2 = 0.0;
+                    if (lane == f) {
+                        sample_piece(c, ts, lo, dt, n, Tb, true, Tr, r2, g2, b2);
+                        rr = r2;
+                        gg = g2;
+                        bb = b2;
+                    }
+                    Tend = __shfl_sync(kFull, Tr, f);
+                    term = true;
+                }
+                Cr += warp_sum(rr);
+                Cg += warp_sum(gg);
+                Cb += warp_sum(bb);
+                T = Tend;
+            } else if (maxn > 0) {
+                composite_balanced(n, lo, dt, ts, c);
             }
         }
         // composited start pieces are dead: their slots return to the pool
@@ -350,6 +378,69 @@ class RayWorker {
         open_t = last_t;
         open_slot = last_slot;
         has_open = true;
+    }
+
+    // Sample-parallel compositing for chunks containing long pieces: samples
+    // are dealt 32 at a time across the lanes, in order.
+    __device__ void composite_balanced(int n, double lo, double dt, int64_t ts,
+                                       const double (&cl)[D + 1]) {
+        const int incl = warp_incl_scan(n, lane);
+        const int total = __shfl_sync(kFull, incl, 31);
+        for (int base = 0; base < total && !term; base += 32) {
+            const int k = base + lane;
+            const bool act = k < total;
+            int lo_l = 0, hi_l = 31;
+#pragma unroll
+            for (int it = 0; it < 5; ++it) {
+                const int mid = (lo_l + hi_l) >> 1;
+                const int v = __shfl_sync(kFull, incl, mid);
+                if (v > k)
+                    hi_l = mid;
+                else
+                    lo_l = mid + 1;
+            }
+            const int j = lo_l;
+            const int s = k - (__shfl_sync(kFull, incl, j) - __shfl_sync(kFull, n, j));
+            const double lo_j = __shfl_sync(kFull, lo, j);
+            const double dt_j = __shfl_sync(kFull, dt, j);
+            const int64_t ts_j = __shfl_sync(kFull, ts, j);
+            double c[D + 1];
+#pragma unroll
+            for (int d = 0; d <= D; ++d) c[d] = __shfl_sync(kFull, cl[d], j);
+            double alpha = 0.0, r = 0.0, g = 0.0, b = 0.0;
+            if (act) {
+                const double t = dadd(lo_j, dmul(dadd(static_cast<double>(s), 0.5), dt_j));
+                const double x = t * P.inv_tau - static_cast<double>(ts_j);
+                double acc = c[D];
+#pragma unroll
+                for (int d = D - 1; d >= 0; --d) acc = fma(acc, x, c[d]);
+                double ab;
+                tf_sample(P.tf, P.ntf, acc * P.Q.sigma, r, g, b, ab);
+                alpha = static_cast<double>(-expm1f(static_cast<float>(-ab * dt_j)));
+            }
+            const double f = act ? 1.0 - alpha : 1.0;
+            double pre = f;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double u = __shfl_up_sync(kFull, pre, o);
+                if (lane >= o) pre *= u;
+            }
+            double excl = __shfl_up_sync(kFull, pre, 1);
+            if (lane == 0) excl = 1.0;
+            const double Tb = T * excl;
+            const unsigned okm = __ballot_sync(kFull, act && Tb > 1e-3);
+            const unsigned actm = __ballot_sync(kFull, act);
+            const unsigned fail = actm & ~okm;
+            const int first_fail = fail ? __ffs(fail) - 1 : 32;
+            const bool inc = act && lane < first_fail;
+            const double ta = inc ? Tb * alpha : 0.0;
+            Cr += warp_sum(inc ? ta * r : 0.0);
+            Cg += warp_sum(inc ? ta * g : 0.0);
+            Cb += warp_sum(inc ? ta * b : 0.0);
+            const unsigned incm = __ballot_sync(kFull, inc);
+            if (incm) T = __shfl_sync(kFull, Tb * f, 31 - __clz(incm));
+            if (fail) term = true;
+        }
     }
 
     // Finalise every pending knot with t < F (all of them if all_): equal
@@ -435,7 +526,7 @@ class RayWorker {
 
     // Quantize the first nq queued hits (lane per hit) and merge their knots
     // into the sorted window.  Returns false if the window is too small.
-    __device__ bool insert_hits(int nq, int64_t F_pre) {
+    __device__ bool insert_hits(int nq) {
         constexpr int R = C::R;
         const bool act = lane < nq;
         int pi = 0;
@@ -458,10 +549,7 @@ class RayWorker {
         const int off = warp_incl_scan(nk, lane) - nk;
         const int total = __shfl_sync(kFull, off + nk, 31);
         if (total == 0) return true;
-        if (total > nfree) {
-            flush(F_pre, false);
-            if (total > nfree) return false;
-        }
+        if (total > nfree) return false;  // the caller flushed; the window is genuinely full
         const int slot0 = nfree - total + off;  // this lane's slots: fl[slot0 .. slot0 + nk)
         int64_t kt[R];
         int ks[R];
@@ -592,10 +680,22 @@ class RayWorker {
                 cursor += 32;
             }
             __syncwarp();
+            // ---- flush: every knot below F is final.  F bounds every knot of
+            // the queued hits and of the untested candidates (depth-sorted).
+            // One call site keeps the kernel's code (and its i-cache
+            // footprint) small.
+            const bool final_ = hq_n == 0 && cursor >= ce;
+            int64_t F = INT64_MAX;
+            if (!final_) {
+                const uint32_t next = hq_n > 0 ? static_cast<uint32_t>(w.hq_c[0]) : cursor;
+                F = knot_floor(P.front[P.cand[next]], P.Q.tau);
+            }
+            if (final_ || nfree < 32 * C::KN || lower_bound64(w.pt, np, F) >= 32) flush(F, final_);
+            if (final_) break;
+            if (term && P.mode == SPHRAY_MODE_FAST) break;
             if (hq_n > 0) {
                 const int nq = hq_n < 32 ? hq_n : 32;
-                const int64_t F_pre = knot_floor(P.front[P.cand[w.hq_c[0]]], P.Q.tau);
-                if (!insert_hits(nq, F_pre)) return false;
+                if (!insert_hits(nq)) return false;
                 const int rest = hq_n - nq;
                 int32_t qc = 0, qp = 0;
                 double ql = 0.0, qt = 0.0;
@@ -615,15 +715,6 @@ class RayWorker {
                 __syncwarp();
                 hq_n = rest;
             }
-            if (hq_n == 0 && cursor >= ce) {
-                flush(0, true);
-                break;
-            }
-            const uint32_t next = hq_n > 0 ? static_cast<uint32_t>(w.hq_c[0]) : cursor;
-            const int64_t F = knot_floor(P.front[P.cand[next]], P.Q.tau);
-            const int nf = lower_bound64(w.pt, np, F);
-            if (nf >= 32 || nfree < 32 * C::KN) flush(F, false);
-            if (term && P.mode == SPHRAY_MODE_FAST) break;
         }
         return true;
     }
