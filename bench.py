@@ -247,16 +247,18 @@ def run_ours(args):
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.5)
-    per_step = []
+    per_step, walls = [], []
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
+        tw = time.perf_counter()
         with torch.cuda.stream(stream):
             flush.fill_(1.0)  # L2 flush (256 MB > 126 MB L2) between frames
         _, st = ctx.render(cam, tf, qc, ds, opts, to_host=False)
         per_step.append(st)
+        walls.append(1e3 * (time.perf_counter() - tw))
     e1.record(stream)
     barrier()
     clocks = sampler.stop()
@@ -340,7 +342,9 @@ def run_ours(args):
             "gpu_launches": int(st.launches) * args.steps,
             "clocks": clocks,
             "breakdown_ms": {"bin": bin_ms, "render_kernel": render_ms,
-                             "frame_device": statistics.median(s.device_ms for s in per_step)},
+                             "frame_device": statistics.median(s.device_ms for s in per_step),
+                             "per_step_device": [round(s.device_ms, 3) for s in per_step],
+                             "per_step_wall": [round(x, 3) for x in walls]},
             "stats": {"hits": st.hits, "knots": st.knots, "rays_touched": st.rays_touched,
                       "candidates": st.candidates, "max_window": st.max_window,
                       "window_retries": st.window_retries, "int_ops": st.int_ops,

@@ -8,7 +8,10 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -247,10 +250,30 @@ int bits_for(uint64_t v) {
 constexpr size_t kSmemLimit = 227 * 1024;
 }  // namespace
 
+namespace {
+// SPHRAY_TRACE=1: host-side phase timings of each frame on stderr
+struct Trace {
+    bool on = std::getenv("SPHRAY_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+    std::string line;
+    void mark(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        line += std::string(" ") + what + "=" +
+                std::to_string(std::chrono::duration<double, std::milli>(now - last).count());
+        last = now;
+    }
+    ~Trace() {
+        if (on) std::fprintf(stderr, "[sphray trace]%s\n", line.c_str());
+    }
+};
+}  // namespace
+
 void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t ntf,
                     const sphray_quanta& qc, const sphray_dataset_stats& ds,
                     const sphray_render_options& opts, double* rgb_host,
                     sphray_render_stats* out, Dumps* dumps) {
+    Trace trace;
     set_device();
     const CamConst C = make_camera(cam);  // render_scene: cam.validate() (raycast.hpp:419)
     validate_tf(tf, ntf);                 // raycast.hpp:420
@@ -322,6 +345,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         CUDA_OK(cudaMemcpyAsync(&tail[0], d_offsets_.as<uint32_t>() + (n - 1), 4, cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaMemcpyAsync(&tail[1], d_counts_.as<uint32_t>() + (n - 1), 4, cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaStreamSynchronize(s));
+        trace.mark("prep+scan");
         entries = static_cast<uint64_t>(tail[0]) + tail[1];
         if (entries >= 0xffffffffull)
             fail(SPHRAY_ERR_CAPACITY, "more than 2^32 (tile, particle) entries; shard over more ranks");
@@ -434,14 +458,23 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         P.mode = SPHRAY_MODE_EXACT;
     }
     int cap = opts.window > 0 ? std::min(opts.window, 65535) : 512;
-    int warps = 4;
-    size_t wb = warp_smem_bytes(D, cap, m);
-    while (warps > 1 && wb * warps > kSmemLimit) --warps;
-    if (wb * warps > kSmemLimit) fail(SPHRAY_ERR_CONFIG, "knot window does not fit shared memory");
+    const size_t wb = warp_smem_bytes(D, cap, m);
+    if (wb > kSmemLimit) fail(SPHRAY_ERR_CONFIG, "knot window does not fit shared memory");
+    // CTA size: the warps-per-CTA that packs the most warps per SM (shared
+    // memory is the occupancy limiter; each warp carries its own window)
+    int warps = 1, bps = 0, best = 0;
+    for (int wpb : {4, 2, 8, 1}) {
+        if (wb * wpb > kSmemLimit) continue;
+        const int nb = max_blocks_per_sm(D, m, wpb, wb * wpb);
+        if (nb * wpb > best) {
+            best = nb * wpb;
+            warps = wpb;
+            bps = nb;
+        }
+    }
+    if (bps < 1) bps = 1;
     P.cap = cap;
     P.warp_bytes = static_cast<int>(wb);
-    int bps = max_blocks_per_sm(D, m, warps, wb * warps);
-    if (bps < 1) bps = 1;
     CUDA_OK(cudaMemsetAsync(d_work_.p, 0, 8, s));
     CUDA_OK(cudaMemsetAsync(d_retry_count_.p, 0, 8, s));
     CUDA_OK(cudaEventRecord(evr0_, s));
@@ -451,9 +484,11 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     }
 
     // ---- rays whose window overflowed: once more with the widest window
+    trace.mark("launch");
     unsigned retry = 0;
     CUDA_OK(cudaMemcpyAsync(&retry, d_retry_count_.p, 4, cudaMemcpyDeviceToHost, s));
     CUDA_OK(cudaStreamSynchronize(s));
+    trace.mark("render");
     if (retry > 0) {
         int cap2 = 65535;
         while (cap2 > cap && warp_smem_bytes(D, cap2, m) > kSmemLimit) cap2 = cap2 * 15 / 16;
@@ -520,6 +555,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         CUDA_OK(cudaEventRecord(ev1_, s));
         CUDA_OK(cudaStreamSynchronize(s));
     }
+    trace.mark("tail");
     float ms = 0.0f, ms_bin = 0.0f, ms_render = 0.0f;
     CUDA_OK(cudaEventElapsedTime(&ms, ev0_, ev1_));
     CUDA_OK(cudaEventElapsedTime(&ms_bin, ev0_, evr0_));

@@ -21,41 +21,50 @@ template <int M>
 struct HitPositions {
     static constexpr int KN = 2 * M + 1;
     int64_t pos[M + 1];  // pos[0] centre, pos[k] positive knots
-    int64_t kpos[KN];       // emission order -m..-1, [0], 1..m (nondecreasing)
-    int nraw;               // emitted entries before the coincident merge
-    int nk;                 // distinct positions (knots actually emitted)
-    const double* row;      // LUT entry: m knots then |J| jumps
+    int64_t kpos[KN];    // emission order -m..-1, [0], 1..m (nondecreasing); odd K: no centre
+    int nraw;            // emitted entries before the coincident merge (2m+1 or 2m)
+    int nk;              // distinct positions (knots actually emitted)
+    const double* row;   // LUT entry: m knots then |J| jumps
 };
 
 // Phase A.  Returns false when quantize_particle emits nothing (lam >= q,
-// quantize.hpp:204).
+// quantize.hpp:204).  All array indices are compile-time (M is a template
+// parameter, the parity of K a runtime select) so nothing spills to local
+// memory.
 template <int M>
 __device__ __forceinline__ bool quantize_positions(const QuantParams& Q, double h, double lam,
                                                    double tchi, HitPositions<M>& hp,
                                                    bool& ovf) {
-    hp.nraw = 0;
+    constexpr int KN = HitPositions<M>::KN;
+    const bool even = (Q.K & 1) == 0;
+    hp.nraw = even ? KN : KN - 1;
     hp.nk = 0;
 #pragma unroll
     for (int k = 0; k <= M; ++k) hp.pos[k] = 0;
+#pragma unroll
+    for (int q = 0; q < KN; ++q) hp.kpos[q] = 0;
     if (!(lam < Q.q)) return false;
     const int e = lut_index(lam, Q.lut_dl, Q.lut_N);
     hp.row = Q.lut_rows + static_cast<size_t>(e) * Q.lut_stride;
     hp.pos[0] = round_checked(ddiv(tchi, Q.tau), ovf);
 #pragma unroll
     for (int k = 1; k <= M; ++k)
-        if (k <= M)
-            hp.pos[k] = cadd(hp.pos[0], round_checked(ddiv(dmul(h, hp.row[k - 1]), Q.tau), ovf), ovf);
+        hp.pos[k] = cadd(hp.pos[0], round_checked(ddiv(dmul(h, hp.row[k - 1]), Q.tau), ovf), ovf);
     const int64_t twice = cadd(hp.pos[0], hp.pos[0], ovf);
+    bool ov2 = false;  // the negative side is evaluated for all k; flags count once
 #pragma unroll
-    for (int k = M; k >= 1; --k)
-        if (k <= M) hp.kpos[hp.nraw++] = csub(twice, hp.pos[k], ovf);  // lut.hpp:150
-    if ((Q.K & 1) == 0) hp.kpos[hp.nraw++] = hp.pos[0];
+    for (int i = 0; i < M; ++i) hp.kpos[i] = csub(twice, hp.pos[M - i], ov2);  // lut.hpp:150
+    ovf |= ov2;
+    // positive side (lut.hpp:154-166): even K puts the centre at index m
 #pragma unroll
-    for (int k = 1; k <= M; ++k)
-        if (k <= M) hp.kpos[hp.nraw++] = hp.pos[k];
+    for (int j = 0; j <= M; ++j) {
+        const int64_t ev = (j == 0) ? hp.pos[0] : hp.pos[j];
+        const int64_t od = (j < M) ? hp.pos[j + 1] : 0;
+        hp.kpos[M + j] = even ? ev : od;
+    }
     hp.nk = 1;
 #pragma unroll
-    for (int q = 1; q < HitPositions<M>::KN; ++q)
+    for (int q = 1; q < KN; ++q)
         if (q < hp.nraw && hp.kpos[q] != hp.kpos[q - 1]) ++hp.nk;
     return true;
 }
@@ -68,6 +77,8 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
                                               const HitPositions<M>& hp, bool& ovf,
                                               Sink&& sink) {
     constexpr int m = M;
+    constexpr int KN = HitPositions<M>::KN;
+    const bool even = (Q.K & 1) == 0;
     int64_t negk[M][D + 1];  // negk[k-1] == bneg[m-k] of lut.hpp:106
     int64_t center[D + 1];
 #pragma unroll
@@ -76,16 +87,15 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
         for (int d = 0; d <= D; ++d) negk[k][d] = 0;
 #pragma unroll
     for (int d = 0; d <= D; ++d) center[d] = 0;
-    const int c1 = (Q.K & 1) ? D / 2 : D;  // index-set entries with k == 1 (approx.hpp:48-51)
+    const int c1 = even ? D : D / 2;  // index-set entries with k == 1 (approx.hpp:48-51)
 #pragma unroll
     for (int k = 1; k <= M; ++k) {
-        if (k > M) continue;
 #pragma unroll
         for (int d = 1; d <= D; ++d) {
             int ii;
             if (k == 1) {
-                if ((Q.K & 1) && (d & 1)) continue;
-                ii = (Q.K & 1) ? d / 2 - 1 : d - 1;
+                if (!even && (d & 1)) continue;
+                ii = even ? d - 1 : d / 2 - 1;
             } else {
                 ii = c1 + (k - 2) * D + (d - 1);
             }
@@ -94,14 +104,13 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
             negk[k - 1][d] = (d & 1) ? bp : cneg(bp, ovf);  // lut.hpp:107-109
         }
     }
-    if ((Q.K & 1) == 0) {
+    if (even) {
         // even K: the centre knot carries the odd-order jumps (lut.hpp:118-130)
 #pragma unroll
         for (int d = 1; d <= D; d += 2) {
             int64_t acc = 0;
 #pragma unroll
             for (int k = 1; k <= M; ++k) {
-                if (k > M) continue;
                 const int64_t off = csub(hp.pos[k], hp.pos[0], ovf);
                 int64_t pw = 1;
 #pragma unroll
@@ -118,11 +127,9 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
         for (int d = (D % 2 == 1 ? D : D - 1); d >= 1; d -= 2) {
             int64_t acc = 0;
 #pragma unroll
-            for (int k = 2; k <= M; ++k)
-                if (k <= m) acc = cadd(acc, negk[k - 1][d], ovf);
+            for (int k = 2; k <= M; ++k) acc = cadd(acc, negk[k - 1][d], ovf);
 #pragma unroll
             for (int k = 1; k <= M; ++k) {
-                if (k > M) continue;
                 const int64_t off = csub(hp.pos[k], hp.pos[0], ovf);
                 int64_t pw = off;
 #pragma unroll
@@ -134,37 +141,43 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
             negk[0][d] = cneg(acc, ovf);
         }
     }
-    // assembly (lut.hpp:147-166) with the coincident merge of quantize.hpp:229-242
+    // jumps in emission order (lut.hpp:147-166), static indices like kpos
+    auto jump = [&](int q, int d) -> int64_t {
+        if (q < M) return negk[M - 1 - q][d];
+        const int j = q - M;  // even: 0 = centre, k = j; odd: k = j + 1
+        if (even) {
+            if (j == 0) return center[d];
+            const int64_t v = negk[j - 1][d];
+            return (d & 1) ? v : static_cast<int64_t>(0ull - static_cast<uint64_t>(v));
+        }
+        if (j + 1 > M) return 0;
+        const int64_t v = negk[j][d];
+        return (d & 1) ? v : static_cast<int64_t>(0ull - static_cast<uint64_t>(v));
+    };
+    // the positive side negates even orders (checked in the reference)
+#pragma unroll
+    for (int k = 1; k <= M; ++k)
+#pragma unroll
+        for (int d = 0; d <= D; d += 2) ovf |= negk[k - 1][d] == INT64_MIN;
+    // coincident merge of quantize.hpp:229-242
     int64_t cur[D + 1];
 #pragma unroll
-    for (int d = 0; d <= D; ++d) cur[d] = 0;
-    int o = 0, q = 0;
-    auto put = [&](const int64_t (&b)[D + 1]) {
-        if (q > 0 && hp.kpos[q] == hp.kpos[q - 1]) {
+    for (int d = 0; d <= D; ++d) cur[d] = jump(0, d);
+    int o = 0;
 #pragma unroll
-            for (int d = 0; d <= D; ++d) cur[d] = cadd(cur[d], b[d], ovf);
-        } else {
-            if (q > 0) sink(o++, hp.kpos[q - 1], cur);
+    for (int q = 1; q < KN; ++q) {
+        if (q < hp.nraw) {
+            if (hp.kpos[q] == hp.kpos[q - 1]) {
 #pragma unroll
-            for (int d = 0; d <= D; ++d) cur[d] = b[d];
+                for (int d = 0; d <= D; ++d) cur[d] = cadd(cur[d], jump(q, d), ovf);
+            } else {
+                sink(o++, hp.kpos[q - 1], cur);
+#pragma unroll
+                for (int d = 0; d <= D; ++d) cur[d] = jump(q, d);
+            }
         }
-        ++q;
-    };
-#pragma unroll
-    for (int k = M; k >= 1; --k) {
-        if (k > M) continue;
-        put(negk[k - 1]);
     }
-    if ((Q.K & 1) == 0) put(center);
-#pragma unroll
-    for (int k = 1; k <= M; ++k) {
-        if (k > M) continue;
-        int64_t b[D + 1];
-#pragma unroll
-        for (int d = 0; d <= D; ++d) b[d] = (d & 1) ? negk[k - 1][d] : cneg(negk[k - 1][d], ovf);
-        put(b);
-    }
-    sink(o, hp.kpos[q - 1], cur);
+    sink(o, even ? hp.kpos[KN - 1] : hp.kpos[KN - 2], cur);
 }
 
 }  // namespace dev

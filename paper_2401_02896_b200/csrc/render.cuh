@@ -27,7 +27,8 @@ SPHRAY_HD inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 SPHRAY_HD inline size_t warp_bytes_for(int D, int cap, int nb) {
     size_t b = 0;
-    b += align16(sizeof(uint64_t) * (D + 1) * cap);
+    b += align16(sizeof(uint64_t) * D * cap);
+    b += align16(sizeof(uint64_t) * 32);
     b += align16(sizeof(int64_t) * cap);
     b += align16(sizeof(int64_t) * nb);
     b += align16(sizeof(double) * kHitQueue * 2);

@@ -156,6 +156,52 @@ __device__ __forceinline__ void bitonic_sort(int64_t (&t)[R], int (&s)[R], int l
     }
 }
 
+// Packed-key variant: one u64 per element, ((t - base) << 16) | slot.  Each
+// lane's R elements arrive already sorted (ascending on even lanes, descending
+// on odd lanes -- exactly the state after the first log2(R) bitonic phases),
+// so the network starts at phase 2R.
+template <int R, int J>
+__device__ __forceinline__ void bitonic_intra_keys(uint64_t (&k)[R], bool asc) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if ((r & J) == 0) {
+            const int r2 = r | J;
+            const uint64_t a = k[r], b = k[r2];
+            const bool sw = asc ? (a > b) : (a < b);
+            k[r] = sw ? b : a;
+            k[r2] = sw ? a : b;
+        }
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void bitonic_sort_keys(uint64_t (&k)[R], int lane) {
+#pragma unroll 1
+    for (int size = 2 * R; size <= 32 * R; size <<= 1) {
+        const bool asc = ((lane * R) & size) == 0;
+#pragma unroll 1
+        for (int stride = size >> 1; stride >= 1; stride >>= 1) {
+            if (stride >= R) {
+                const int ls = stride / R;
+                const bool keep_min = ((lane & ls) == 0) == asc;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const uint64_t o = __shfl_xor_sync(kFull, k[r], ls);
+                    k[r] = (keep_min == (o < k[r])) ? o : k[r];
+                }
+            } else if (stride == 8 && R > 8) {
+                bitonic_intra_keys<R, (R > 8 ? 8 : 1)>(k, asc);
+            } else if (stride == 4) {
+                bitonic_intra_keys<R, 4>(k, asc);
+            } else if (stride == 2) {
+                bitonic_intra_keys<R, 2>(k, asc);
+            } else {
+                bitonic_intra_keys<R, 1>(k, asc);
+            }
+        }
+    }
+}
+
 constexpr int kLaneSamples = 8;  // pieces up to this many samples are sampled lane-locally
 
 template <int M>
@@ -166,7 +212,8 @@ struct Cfg {
 };
 
 struct WarpMem {
-    uint64_t* pool;  // (D+1) x cap, SoA: jumps while pending, merged coefficients once a piece
+    uint64_t* pool;  // D x cap, SoA: jumps (orders 1..D) while pending, merged coefficients once a piece
+    uint64_t* na0;   // 32: order-0 coefficients of the pieces staged in nt/ns
     int64_t* pt;     // pending knot positions, sorted ascending
     int64_t* nt;     // staging: sorted new knots / the pieces of a chunk
     double* hq_lam;  // hit queue (candidate order)
@@ -180,10 +227,13 @@ struct WarpMem {
 
 
 __device__ inline WarpMem carve(char* base, int D, int cap, int nb) {
+    // layout must match warp_bytes_for (render.cuh)
     WarpMem w;
     char* p = base;
     w.pool = reinterpret_cast<uint64_t*>(p);
-    p += align16(sizeof(uint64_t) * (D + 1) * cap);
+    p += align16(sizeof(uint64_t) * D * cap);
+    w.na0 = reinterpret_cast<uint64_t*>(p);
+    p += align16(sizeof(uint64_t) * 32);
     w.pt = reinterpret_cast<int64_t*>(p);
     p += align16(sizeof(int64_t) * cap);
     w.nt = reinterpret_cast<int64_t*>(p);
@@ -217,6 +267,7 @@ class RayWorker {
     bool has_ref = false;
     int64_t open_t = 0;  // last piece: its successor is not known yet
     int open_slot = 0;
+    uint64_t open_a0 = 0;  // order-0 coefficient of the open piece (slots hold orders 1..D)
     bool has_open = false;
     double T = 1.0, Cr = 0.0, Cg = 0.0, Cb = 0.0;
     bool term = false;
@@ -235,6 +286,7 @@ class RayWorker {
         has_ref = false;
         open_t = 0;
         open_slot = 0;
+        open_a0 = 0;
         has_open = false;
         T = 1.0;
         Cr = Cg = Cb = 0.0;
@@ -292,18 +344,22 @@ class RayWorker {
         const bool have = lane < cp && (lane > 0 || has_open);
         int64_t ts = 0, te = 0;
         int slot = 0;
+        uint64_t a0 = 0;
         if (lane < cp) {
             te = w.nt[lane];
             if (lane == 0) {
                 ts = open_t;
                 slot = open_slot;
+                a0 = open_a0;
             } else {
                 ts = w.nt[lane - 1];
                 slot = w.ns[lane - 1];
+                a0 = w.na0[lane - 1];
             }
         }
         const int last_slot = __shfl_sync(kFull, lane < cp ? static_cast<int>(w.ns[lane]) : 0, cp - 1);
         const int64_t last_t = __shfl_sync(kFull, te, cp - 1);
+        const uint64_t last_a0 = __shfl_sync(kFull, lane < cp ? w.na0[lane] : 0ull, cp - 1);
 
         if (!term) {
             int n = 0;
@@ -321,10 +377,11 @@ class RayWorker {
                     const double cc = ceil(ddiv(dsub(hi, lo), P.step));
                     n = cc > 2.0 ? static_cast<int>(cc) : 2;
                     dt = ddiv(dsub(hi, lo), static_cast<double>(n));
-                    bool zero = true;
+                    bool zero = a0 == 0;
+                    c[0] = static_cast<double>(static_cast<int64_t>(a0));
 #pragma unroll
-                    for (int d = 0; d <= D; ++d) {
-                        const int64_t a = static_cast<int64_t>(w.pool[d * P.cap + slot]);
+                    for (int d = 1; d <= D; ++d) {
+                        const int64_t a = static_cast<int64_t>(w.pool[(d - 1) * P.cap + slot]);
                         zero &= a == 0;
                         c[d] = static_cast<double>(a);
                     }
@@ -377,6 +434,7 @@ class RayWorker {
         free_slots(have, slot);
         open_t = last_t;
         open_slot = last_slot;
+        open_a0 = last_a0;
         has_open = true;
     }
 
@@ -468,7 +526,9 @@ class RayWorker {
             }
             uint64_t g[D + 1];
 #pragma unroll
-            for (int d = 0; d <= D; ++d) g[d] = valid ? w.pool[d * P.cap + s] : 0ull;
+            g[0] = 0ull;  // b_0 == 0 for every knot
+#pragma unroll
+            for (int d = 1; d <= D; ++d) g[d] = valid ? w.pool[(d - 1) * P.cap + s] : 0ull;
             taylor_shift<D>(g, static_cast<uint64_t>(tref) - static_cast<uint64_t>(t));
 #pragma unroll
             for (int d = 0; d <= D; ++d) {
@@ -480,10 +540,11 @@ class RayWorker {
             if (last) {
                 taylor_shift<D>(g, static_cast<uint64_t>(t) - static_cast<uint64_t>(tref));
 #pragma unroll
-                for (int d = 0; d <= D; ++d) w.pool[d * P.cap + s] = g[d];
+                for (int d = 1; d <= D; ++d) w.pool[(d - 1) * P.cap + s] = g[d];
                 const int pr = __popc(pm & lanemask_lt());
                 w.nt[pr] = t;
                 w.ns[pr] = static_cast<uint16_t>(s);
+                w.na0[pr] = g[0];
                 if (P.dump_piece_t) {
                     const unsigned long long at = atomicAdd(&P.dump_count[1], 1ull);
                     if (at < P.dump_cap_pieces) {
@@ -556,8 +617,9 @@ class RayWorker {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             kt[r] = INT64_MAX;
-            ks[r] = 0;
+            ks[r] = -1;  // padding marker
         }
+        const bool odd = lane & 1;
         if (emits) {
             double X[2 * D];
             const double* xs = P.xy + static_cast<size_t>(pi) * (2 * D);
@@ -565,11 +627,13 @@ class RayWorker {
             for (int d = 0; d < 2 * D; ++d) X[d] = xs[d];
             quantize_emit<D, M>(P.Q, X, hp, ovf, [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
                 const int slot = w.fl[slot0 + o];
+                // b[0] is structurally zero (lut.hpp:107-166): only orders 1..D are stored
 #pragma unroll
-                for (int d = 0; d <= D; ++d) w.pool[d * P.cap + slot] = static_cast<uint64_t>(b[d]);
+                for (int d = 1; d <= D; ++d) w.pool[(d - 1) * P.cap + slot] = static_cast<uint64_t>(b[d]);
+                const int at = odd ? R - 1 - o : o;  // odd lanes hold a descending block
 #pragma unroll
                 for (int r = 0; r < R; ++r)
-                    if (r == o) {
+                    if (r == at) {
                         kt[r] = t;
                         ks[r] = slot;
                     }
@@ -579,9 +643,33 @@ class RayWorker {
         __syncwarp();
         nfree -= total;
 
-        // sort the new knots, then merge them into the window in place:
-        // pending elements move up (highest chunk first), new ones fill the gaps
-        bitonic_sort<R>(kt, ks, lane);
+        // sort the new knots.  Packed keys when the batch spans < 2^47 tau
+        // (always, in practice); the (t, slot) pair network otherwise.
+        int64_t lo_t = emits ? hp.kpos[0] : INT64_MAX;
+        int64_t hi_t = emits ? hp.pos[M] : INT64_MIN;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int64_t a = __shfl_xor_sync(kFull, lo_t, o);
+            const int64_t b = __shfl_xor_sync(kFull, hi_t, o);
+            lo_t = a < lo_t ? a : lo_t;
+            hi_t = b > hi_t ? b : hi_t;
+        }
+        if (static_cast<uint64_t>(hi_t) - static_cast<uint64_t>(lo_t) < (1ull << 47) && hi_t >= lo_t) {
+            uint64_t key[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                key[r] = ks[r] < 0 ? ~0ull
+                                   : ((static_cast<uint64_t>(kt[r]) - static_cast<uint64_t>(lo_t)) << 16) |
+                                         static_cast<uint64_t>(ks[r]);
+            bitonic_sort_keys<R>(key, lane);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                kt[r] = static_cast<int64_t>(static_cast<uint64_t>(lo_t) + (key[r] >> 16));
+                ks[r] = static_cast<int>(key[r] & 0xffffu);
+            }
+        } else {
+            bitonic_sort<R>(kt, ks, lane);
+        }
         int dB[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -736,7 +824,8 @@ class RayWorker {
             bool residual = false;  // raycast.hpp:477-480: trailing piece must be zero
             if (knots > 0 && complete && has_open) {
 #pragma unroll
-                for (int d = 0; d <= D; ++d) residual |= w.pool[d * P.cap + open_slot] != 0;
+                for (int d = 1; d <= D; ++d) residual |= w.pool[(d - 1) * P.cap + open_slot] != 0;
+                residual |= open_a0 != 0;
             }
             // RayAccumulator op count for P distinct positions (raycast.hpp:217-244)
             const unsigned long long Pp = pieces;
@@ -756,7 +845,7 @@ class RayWorker {
 };
 
 template <int D, int M>
-__global__ void __launch_bounds__(256) k_render_rays(const FrameParams P) {
+__global__ void __maxnreg__(168) k_render_rays(const FrameParams P) {
     extern __shared__ __align__(16) char smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
