@@ -240,13 +240,15 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up (also JIT/first-touch of every buffer)
+    # warm-up (also module loading / first touch of every buffer, the flush included)
     for _ in range(args.warmup):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
         _, st = ctx.render(cam, tf, qc, ds, opts, to_host=False)
 
     sampler = ClockSampler(local)
     sampler.start()
-    time.sleep(0.5)
+    time.sleep(1.0)
     per_step, walls = [], []
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)

@@ -293,9 +293,18 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     const int n = static_cast<int>(n_);
     cudaStream_t s = stream_;
 
-    // per-frame uploads: TF, pow(tau, d) (glibc, quantize.hpp:221)
-    d_tf_.ensure(ntf * 5 * sizeof(double));
-    CUDA_OK(cudaMemcpyAsync(d_tf_.p, tf, ntf * 5 * sizeof(double), cudaMemcpyHostToDevice, s));
+    // per-frame uploads: TF (+ segment inverse widths), pow(tau, d) (glibc, quantize.hpp:221)
+    h_tf_.assign(ntf * 6, 0.0);
+    for (size_t i = 0; i < ntf; ++i) {
+        h_tf_[i * 6 + 0] = tf[i].value;
+        h_tf_[i * 6 + 1] = tf[i].r;
+        h_tf_[i * 6 + 2] = tf[i].g;
+        h_tf_[i * 6 + 3] = tf[i].b;
+        h_tf_[i * 6 + 4] = tf[i].absorption;
+        h_tf_[i * 6 + 5] = i + 1 < ntf ? 1.0 / (tf[i + 1].value - tf[i].value) : 0.0;
+    }
+    d_tf_.ensure(h_tf_.size() * sizeof(double));
+    CUDA_OK(cudaMemcpyAsync(d_tf_.p, h_tf_.data(), h_tf_.size() * sizeof(double), cudaMemcpyHostToDevice, s));
     double powtau[kMaxDegree];
     for (int d = 1; d <= D; ++d) powtau[d - 1] = std::pow(qc.tau, d);
     d_powtau_.ensure(sizeof(powtau));
@@ -414,6 +423,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     P.rank = rank_;
     P.nranks = nranks_;
     P.inv_tau = 1.0 / qc.tau;
+    P.inv_step = 1.0 / step;
     P.tf = d_tf_.as<double>();
     P.ntf = static_cast<int>(ntf);
     P.tf0_clear = tf_absorption_at_zero(tf, ntf) == 0.0;

@@ -92,6 +92,7 @@ class Engine {
         d_dump_pa_, d_stats_all_;
     HostPinned h_stage_;
     std::vector<double> h_powh_;
+    std::vector<double> h_tf_;
 };
 
 }  // namespace sphray_b200

@@ -204,9 +204,8 @@ void launch_quantize_hits_t(const QuantParams& Q, const sphray_particle* ps, con
     } while (0)
 
 size_t warp_smem_bytes(int D, int cap, int mm) {
-    const int kn = 2 * mm + 1;
-    const int R = kn <= 8 ? 8 : 16;
-    return warp_bytes_for(D, cap, 32 * R);
+    (void)mm;
+    return warp_bytes_for(D, cap);
 }
 
 // Every (D, m) the reference admits: D in [1,6], m = ceil(K/2) in [1,4]

@@ -25,16 +25,14 @@ constexpr int kMaxJ = kMaxM * kMaxDegree;
 // Shared-memory bytes of one warp's knot window (layout: render_kernel.cuh carve()).
 SPHRAY_HD inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-SPHRAY_HD inline size_t warp_bytes_for(int D, int cap, int nb) {
+SPHRAY_HD inline size_t warp_bytes_for(int D, int cap) {
     size_t b = 0;
-    b += align16(sizeof(uint64_t) * D * cap);
-    b += align16(sizeof(uint64_t) * 32);
-    b += align16(sizeof(int64_t) * cap);
-    b += align16(sizeof(int64_t) * nb);
-    b += align16(sizeof(double) * kHitQueue * 2);
+    b += align16(sizeof(uint64_t) * (D + 1) * cap);  // pool: t + orders 1..D
+    b += align16(sizeof(uint64_t) * 32);              // na0
+    b += align16(sizeof(double) * kHitQueue * 2);     // hit queue
     b += align16(sizeof(int32_t) * kHitQueue * 2);
-    b += align16(sizeof(uint16_t) * cap * 2);
-    b += align16(sizeof(uint16_t) * nb);
+    b += align16(sizeof(uint16_t) * cap * 3);         // ps, fl, fs
+    b += align16(sizeof(uint16_t) * 32);              // pcs
     return b;
 }
 
@@ -64,9 +62,10 @@ struct FrameParams {
     const uint32_t* tile_end;
     int tiles_x, tiles_y;
     int rank, nranks;
-    double inv_tau;  // 1 / tau for sample abscissae (compositing only)
+    double inv_tau;   // 1 / tau for sample abscissae (compositing only)
+    double inv_step;  // 1 / step (sample counts, checked against the exact quotient)
     // transfer function (raycast.hpp:313-338)
-    const double* tf;  // ntf * 5
+    const double* tf;  // ntf * 6: value, r, g, b, absorption, 1/(next value - value)
     int ntf;
     int tf0_clear;  // tf.sample(0).absorption == 0: zero pieces are exact no-ops
     double step;

@@ -2,6 +2,15 @@
 // explicit-hit quantization kernel, as templates over (D, m).  Each
 // render_d<D>.cu instantiates them for one degree so the 24 (D, m) variants
 // compile in parallel.  See render.cu for the reference mapping.
+//
+// Per-ray knot window (shared memory, one per warp):
+//   pool   (D+1) x cap u64: row 0 = knot position t, rows 1..D = the knot's
+//          jumps (order 0 is structurally zero) -- or, once the knot has
+//          become a FieldPiece, its merged coefficients of orders 1..D
+//   ps     pending knots (slot ids), UNSORTED: inserting a batch is an append
+//   fs     the flush set: pending knots with t < F, selected by a ballot scan
+//          and sorted (packed-key warp bitonic) only when they are final
+//   fl     free-slot stack;  pcs/na0  the pieces of one 32-knot chunk
 #pragma once
 
 #include <cuda_runtime.h>
@@ -39,30 +48,6 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-__device__ __forceinline__ int lower_bound64(const int64_t* a, int n, int64_t x) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (a[mid] < x)
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    return lo;
-}
-
-__device__ __forceinline__ int upper_bound64(const int64_t* a, int n, int64_t x) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (a[mid] <= x)
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    return lo;
-}
-
 // floor(front / tau) - 2: every knot of a not-yet-inserted candidate has
 // t >= this (front is a conservative bound, see dev::front_bound).
 __device__ __forceinline__ int64_t knot_floor(float front, double tau) {
@@ -72,7 +57,12 @@ __device__ __forceinline__ int64_t knot_floor(float front, double tau) {
     return static_cast<int64_t>(v);
 }
 
-// TransferFunction::sample (raycast.hpp:326-337).
+// TransferFunction::sample (raycast.hpp:326-337).  The device TF holds 6
+// doubles per point: value, r, g, b, absorption, 1/(next value - value), so
+// the interpolation weight (v - a.value)/(b.value - a.value) is one multiply
+// (<= 1 ulp from the reference's division; inside the RGB tolerance).
+constexpr int kTfStride = 6;
+
 __device__ __forceinline__ void tf_sample(const double* tf, int n, double v, double& r, double& g,
                                           double& b, double& ab) {
     if (v <= tf[0]) {
@@ -82,7 +72,7 @@ __device__ __forceinline__ void tf_sample(const double* tf, int n, double v, dou
         ab = tf[4];
         return;
     }
-    const double* last = tf + 5 * (n - 1);
+    const double* last = tf + kTfStride * (n - 1);
     if (v >= last[0]) {
         r = last[1];
         g = last[2];
@@ -91,42 +81,51 @@ __device__ __forceinline__ void tf_sample(const double* tf, int n, double v, dou
         return;
     }
     int i = 1;
-    while (tf[5 * i] < v) ++i;
-    const double* A = tf + 5 * (i - 1);
-    const double* B = tf + 5 * i;
-    const double w = ddiv(dsub(v, A[0]), dsub(B[0], A[0]));
-    r = dadd(A[1], dmul(w, dsub(B[1], A[1])));
-    g = dadd(A[2], dmul(w, dsub(B[2], A[2])));
-    b = dadd(A[3], dmul(w, dsub(B[3], A[3])));
-    ab = dadd(A[4], dmul(w, dsub(B[4], A[4])));
+    while (tf[kTfStride * i] < v) ++i;
+    const double* A = tf + kTfStride * (i - 1);
+    const double* B = A + kTfStride;
+    const double w = (v - A[0]) * A[5];
+    r = fma(w, B[1] - A[1], A[1]);
+    g = fma(w, B[2] - A[2], A[2]);
+    b = fma(w, B[3] - A[3], A[3]);
+    ab = fma(w, B[4] - A[4], A[4]);
 }
 
-// Warp bitonic sort of 32*R (t, slot) pairs held R per lane (blocked layout:
-// element e = lane*R + r).  Ascending in t; equal t may end in any order
-// (their jumps are summed).  The (size, stride) stage loop is
-// a runtime loop so the code stays small (the render kernel is instruction-
-// cache bound when this is fully unrolled); only the per-register bodies are
-// unrolled: one cross-lane body and one intra-lane body per stride < R.
+// n = max(2, ceil((hi - lo) / step)) exactly as the reference counts samples
+// (raycast.hpp:367): a multiply by 1/step, with the exact division only when
+// the quotient is within rounding distance of an integer.
+__device__ __forceinline__ int sample_count(double len, double step, double inv_step) {
+    const double q = len * inv_step;
+    double c = ceil(q);
+    if (fabs(q - rint(q)) <= 1e-12 * q + 1e-300) c = ceil(ddiv(len, step));
+    return c > 2.0 ? static_cast<int>(c) : 2;
+}
+
+constexpr int kLaneSamples = 8;  // pieces up to this many samples are sampled lane-locally
+__constant__ double c_inv_small[kLaneSamples + 1] = {0.0, 1.0, 1.0 / 2, 1.0 / 3, 1.0 / 4,
+                                                     1.0 / 5, 1.0 / 6, 1.0 / 7, 1.0 / 8};
+
+// Warp bitonic sort of 32*R u64 keys held R per lane (blocked layout:
+// element e = lane*R + r), ascending.  The (size, stride) stage loop is a
+// runtime loop so the code stays small (the kernel is instruction-cache
+// sensitive); only the per-register bodies are unrolled.
 template <int R, int J>
-__device__ __forceinline__ void bitonic_intra(int64_t (&t)[R], int (&s)[R], int lane, int size) {
+__device__ __forceinline__ void bitonic_intra(uint64_t (&k)[R], int lane, int size) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         if ((r & J) == 0) {
             const int r2 = r | J;
             const bool asc = (((lane * R) + r) & size) == 0;
-            const bool sw = asc ? (t[r] > t[r2]) : (t[r] < t[r2]);
-            const int64_t a = t[r], b = t[r2];
-            const int sa = s[r], sb = s[r2];
-            t[r] = sw ? b : a;
-            t[r2] = sw ? a : b;
-            s[r] = sw ? sb : sa;
-            s[r2] = sw ? sa : sb;
+            const uint64_t a = k[r], b = k[r2];
+            const bool sw = asc ? (a > b) : (a < b);
+            k[r] = sw ? b : a;
+            k[r2] = sw ? a : b;
         }
     }
 }
 
 template <int R>
-__device__ __forceinline__ void bitonic_sort(int64_t (&t)[R], int (&s)[R], int lane) {
+__device__ __forceinline__ void bitonic_sort(uint64_t (&k)[R], int lane) {
 #pragma unroll 1
     for (int size = 2; size <= 32 * R; size <<= 1) {
 #pragma unroll 1
@@ -137,107 +136,43 @@ __device__ __forceinline__ void bitonic_sort(int64_t (&t)[R], int (&s)[R], int l
                 const bool keep_min = ((lane & ls) == 0) == asc;
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    const int64_t ot = __shfl_xor_sync(kFull, t[r], ls);
-                    const int os = __shfl_xor_sync(kFull, s[r], ls);
-                    const bool take = keep_min ? (ot < t[r]) : (ot > t[r]);
-                    t[r] = take ? ot : t[r];
-                    s[r] = take ? os : s[r];
-                }
-            } else if (stride == 8 && R > 8) {
-                bitonic_intra<R, (R > 8 ? 8 : 1)>(t, s, lane, size);
-            } else if (stride == 4) {
-                bitonic_intra<R, 4>(t, s, lane, size);
-            } else if (stride == 2) {
-                bitonic_intra<R, 2>(t, s, lane, size);
-            } else {
-                bitonic_intra<R, 1>(t, s, lane, size);
-            }
-        }
-    }
-}
-
-// Packed-key variant: one u64 per element, ((t - base) << 16) | slot.  Each
-// lane's R elements arrive already sorted (ascending on even lanes, descending
-// on odd lanes -- exactly the state after the first log2(R) bitonic phases),
-// so the network starts at phase 2R.
-template <int R, int J>
-__device__ __forceinline__ void bitonic_intra_keys(uint64_t (&k)[R], bool asc) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        if ((r & J) == 0) {
-            const int r2 = r | J;
-            const uint64_t a = k[r], b = k[r2];
-            const bool sw = asc ? (a > b) : (a < b);
-            k[r] = sw ? b : a;
-            k[r2] = sw ? a : b;
-        }
-    }
-}
-
-template <int R>
-__device__ __forceinline__ void bitonic_sort_keys(uint64_t (&k)[R], int lane) {
-#pragma unroll 1
-    for (int size = 2 * R; size <= 32 * R; size <<= 1) {
-        const bool asc = ((lane * R) & size) == 0;
-#pragma unroll 1
-        for (int stride = size >> 1; stride >= 1; stride >>= 1) {
-            if (stride >= R) {
-                const int ls = stride / R;
-                const bool keep_min = ((lane & ls) == 0) == asc;
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
                     const uint64_t o = __shfl_xor_sync(kFull, k[r], ls);
                     k[r] = (keep_min == (o < k[r])) ? o : k[r];
                 }
-            } else if (stride == 8 && R > 8) {
-                bitonic_intra_keys<R, (R > 8 ? 8 : 1)>(k, asc);
-            } else if (stride == 4) {
-                bitonic_intra_keys<R, 4>(k, asc);
-            } else if (stride == 2) {
-                bitonic_intra_keys<R, 2>(k, asc);
+            } else if (R > 8 && stride == 8) {
+                bitonic_intra<R, (R > 8 ? 8 : 1)>(k, lane, size);
+            } else if (R > 4 && stride == 4) {
+                bitonic_intra<R, (R > 4 ? 4 : 1)>(k, lane, size);
+            } else if (R > 2 && stride == 2) {
+                bitonic_intra<R, (R > 2 ? 2 : 1)>(k, lane, size);
             } else {
-                bitonic_intra_keys<R, 1>(k, asc);
+                bitonic_intra<R, 1>(k, lane, size);
             }
         }
     }
 }
 
-constexpr int kLaneSamples = 8;  // pieces up to this many samples are sampled lane-locally
-
-template <int M>
-struct Cfg {
-    static constexpr int KN = 2 * M + 1;
-    static constexpr int R = KN <= 8 ? 8 : 16;
-    static constexpr int NB = 32 * R;
-};
-
 struct WarpMem {
-    uint64_t* pool;  // D x cap, SoA: jumps (orders 1..D) while pending, merged coefficients once a piece
-    uint64_t* na0;   // 32: order-0 coefficients of the pieces staged in nt/ns
-    int64_t* pt;     // pending knot positions, sorted ascending
-    int64_t* nt;     // staging: sorted new knots / the pieces of a chunk
+    uint64_t* pool;  // (D+1) x cap, SoA (see the file comment)
+    uint64_t* na0;   // 32: order-0 coefficients of the pieces of a chunk
     double* hq_lam;  // hit queue (candidate order)
     double* hq_t;
     int32_t* hq_c;
     int32_t* hq_p;
-    uint16_t* ps;  // pending slots
-    uint16_t* fl;  // free slot stack
-    uint16_t* ns;  // staging slots
+    uint16_t* ps;   // pending slots, unsorted
+    uint16_t* fl;   // free slot stack
+    uint16_t* fs;   // flush set slots (sorted by t)
+    uint16_t* pcs;  // 32: slots of the pieces of a chunk
 };
 
-
-__device__ inline WarpMem carve(char* base, int D, int cap, int nb) {
+__device__ inline WarpMem carve(char* base, int D, int cap) {
     // layout must match warp_bytes_for (render.cuh)
     WarpMem w;
     char* p = base;
     w.pool = reinterpret_cast<uint64_t*>(p);
-    p += align16(sizeof(uint64_t) * D * cap);
+    p += align16(sizeof(uint64_t) * (D + 1) * cap);
     w.na0 = reinterpret_cast<uint64_t*>(p);
     p += align16(sizeof(uint64_t) * 32);
-    w.pt = reinterpret_cast<int64_t*>(p);
-    p += align16(sizeof(int64_t) * cap);
-    w.nt = reinterpret_cast<int64_t*>(p);
-    p += align16(sizeof(int64_t) * nb);
     w.hq_lam = reinterpret_cast<double*>(p);
     w.hq_t = w.hq_lam + kHitQueue;
     p += align16(sizeof(double) * kHitQueue * 2);
@@ -246,8 +181,9 @@ __device__ inline WarpMem carve(char* base, int D, int cap, int nb) {
     p += align16(sizeof(int32_t) * kHitQueue * 2);
     w.ps = reinterpret_cast<uint16_t*>(p);
     w.fl = w.ps + cap;
-    p += align16(sizeof(uint16_t) * cap * 2);
-    w.ns = reinterpret_cast<uint16_t*>(p);
+    w.fs = w.fl + cap;
+    p += align16(sizeof(uint16_t) * cap * 3);
+    w.pcs = reinterpret_cast<uint16_t*>(p);
     return w;
 }
 
@@ -255,7 +191,7 @@ __device__ inline WarpMem carve(char* base, int D, int cap, int nb) {
 template <int D, int M>
 class RayWorker {
    public:
-    using C = Cfg<M>;
+    static constexpr int KN = 2 * M + 1;  // knots per hit, at most
     const FrameParams& P;
     WarpMem w;
     int lane;
@@ -265,9 +201,8 @@ class RayWorker {
     uint64_t G[D + 1];  // running sum of jumps shifted to tref (mod 2^64)
     int64_t tref = 0;
     bool has_ref = false;
-    int64_t open_t = 0;  // last piece: its successor is not known yet
-    int open_slot = 0;
-    uint64_t open_a0 = 0;  // order-0 coefficient of the open piece (slots hold orders 1..D)
+    int open_slot = 0;     // last piece: its successor is not known yet
+    uint64_t open_a0 = 0;  // its order-0 coefficient (the slot holds orders 1..D)
     bool has_open = false;
     double T = 1.0, Cr = 0.0, Cg = 0.0, Cb = 0.0;
     bool term = false;
@@ -275,6 +210,13 @@ class RayWorker {
     int max_pending = 0;
 
     __device__ RayWorker(const FrameParams& p, WarpMem wm, int l) : P(p), w(wm), lane(l) {}
+
+    __device__ __forceinline__ int64_t pool_t(int slot) const {
+        return static_cast<int64_t>(w.pool[slot]);
+    }
+    __device__ __forceinline__ uint64_t& pool_c(int d, int slot) const {
+        return w.pool[d * P.cap + slot];
+    }
 
     __device__ void reset() {
         np = 0;
@@ -284,7 +226,6 @@ class RayWorker {
         for (int d = 0; d <= D; ++d) G[d] = 0;
         tref = 0;
         has_ref = false;
-        open_t = 0;
         open_slot = 0;
         open_a0 = 0;
         has_open = false;
@@ -312,12 +253,13 @@ class RayWorker {
     // the reference's T > 1e-3 check runs before every sample.
     __device__ __forceinline__ void sample_piece(const double (&c)[D + 1], int64_t ts, double lo,
                                                  double dt, int n, double T0, bool stop,
-                                                 double& T, double& cr, double& cg, double& cb) const {
-        T = T0;
+                                                 double& Tout, double& cr, double& cg,
+                                                 double& cb) const {
+        Tout = T0;
         cr = cg = cb = 0.0;
         const double tsd = static_cast<double>(ts);
         for (int s = 0; s < n; ++s) {
-            if (stop && !(T > 1e-3)) break;
+            if (stop && !(Tout > 1e-3)) break;
             const double t = dadd(lo, dmul(dadd(static_cast<double>(s), 0.5), dt));
             const double x = t * P.inv_tau - tsd;
             double acc = c[D];
@@ -326,17 +268,17 @@ class RayWorker {
             double r, g, b, ab;
             tf_sample(P.tf, P.ntf, acc * P.Q.sigma, r, g, b, ab);
             const double alpha = static_cast<double>(-expm1f(static_cast<float>(-ab * dt)));
-            const double ta = T * alpha;
+            const double ta = Tout * alpha;
             cr = fma(ta, r, cr);
             cg = fma(ta, g, cg);
             cb = fma(ta, b, cb);
-            T = T * (1.0 - alpha);
+            Tout = Tout * (1.0 - alpha);
         }
     }
 
     // Composite the pieces completed in this chunk: lane j (j < cp) takes the
     // piece that starts at the previous piece (the carried open piece for
-    // j == 0) and ends at staged piece j.  Each lane samples its own piece
+    // j == 0) and ends at chunk piece j.  Each lane samples its own piece
     // sequentially; one warp combine (prefix product of transmittances,
     // weighted colour sum) then folds the chunk into the ray.  Pieces with
     // many samples (long gaps) go through a sample-parallel path instead.
@@ -346,19 +288,12 @@ class RayWorker {
         int slot = 0;
         uint64_t a0 = 0;
         if (lane < cp) {
-            te = w.nt[lane];
-            if (lane == 0) {
-                ts = open_t;
-                slot = open_slot;
-                a0 = open_a0;
-            } else {
-                ts = w.nt[lane - 1];
-                slot = w.ns[lane - 1];
-                a0 = w.na0[lane - 1];
-            }
+            te = pool_t(w.pcs[lane]);
+            slot = lane == 0 ? open_slot : w.pcs[lane - 1];
+            a0 = lane == 0 ? open_a0 : w.na0[lane - 1];
+            ts = pool_t(slot);
         }
-        const int last_slot = __shfl_sync(kFull, lane < cp ? static_cast<int>(w.ns[lane]) : 0, cp - 1);
-        const int64_t last_t = __shfl_sync(kFull, te, cp - 1);
+        const int last_slot = __shfl_sync(kFull, lane < cp ? static_cast<int>(w.pcs[lane]) : 0, cp - 1);
         const uint64_t last_a0 = __shfl_sync(kFull, lane < cp ? w.na0[lane] : 0ull, cp - 1);
 
         if (!term) {
@@ -374,14 +309,14 @@ class RayWorker {
                 lo = (a_lo < P.cam.near_plane) ? P.cam.near_plane : a_lo;
                 const double hi = (P.cam.far_plane < a_hi) ? P.cam.far_plane : a_hi;
                 if (hi > lo) {
-                    const double cc = ceil(ddiv(dsub(hi, lo), P.step));
-                    n = cc > 2.0 ? static_cast<int>(cc) : 2;
-                    dt = ddiv(dsub(hi, lo), static_cast<double>(n));
+                    const double len = dsub(hi, lo);
+                    n = sample_count(len, P.step, P.inv_step);
+                    dt = n <= kLaneSamples ? len * c_inv_small[n] : len / static_cast<double>(n);
                     bool zero = a0 == 0;
                     c[0] = static_cast<double>(static_cast<int64_t>(a0));
 #pragma unroll
                     for (int d = 1; d <= D; ++d) {
-                        const int64_t a = static_cast<int64_t>(w.pool[(d - 1) * P.cap + slot]);
+                        const int64_t a = static_cast<int64_t>(pool_c(d, slot));
                         zero &= a == 0;
                         c[d] = static_cast<double>(a);
                     }
@@ -432,7 +367,6 @@ class RayWorker {
         }
         // composited start pieces are dead: their slots return to the pool
         free_slots(have, slot);
-        open_t = last_t;
         open_slot = last_slot;
         open_a0 = last_a0;
         has_open = true;
@@ -501,34 +435,111 @@ class RayWorker {
         }
     }
 
-    // Finalise every pending knot with t < F (all of them if all_): equal
-    // positions merge, the running polynomial is the prefix sum of the jumps
-    // Taylor-shifted to a common origin tref (exact modulo 2^64, so equal to
-    // RayAccumulator's Int128 result whenever that fits int64), and each
-    // distinct position becomes a FieldPiece.
-    __device__ void flush(int64_t F, bool all_) {
-        const int nf = all_ ? np : lower_bound64(w.pt, np, F);
-        if (nf == 0) return;
-        for (int c0 = 0; c0 < nf; c0 += 32) {
-            const int i = c0 + lane;
-            const bool valid = i < nf;
-            int64_t t = 0;
-            int s = 0;
-            bool last = false;
-            if (valid) {
-                t = w.pt[i];
-                s = w.ps[i];
-                last = (i == nf - 1) || (w.pt[i + 1] != t);
+    // Sort fs[0, nsel) by knot position: packed u64 keys ((t - tmin) << 16 | slot)
+    // in registers for the usual sizes, an exact rank sort otherwise.
+    template <int R>
+    __device__ void sort_flush_reg(int nsel, int64_t tmin) {
+        uint64_t key[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = lane * R + r;
+            key[r] = ~0ull;
+            if (e < nsel) {
+                const int s = w.fs[e];
+                key[r] = ((static_cast<uint64_t>(pool_t(s)) - static_cast<uint64_t>(tmin)) << 16) |
+                         static_cast<uint64_t>(s);
             }
+        }
+        bitonic_sort<R>(key, lane);
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = lane * R + r;
+            if (e < nsel) w.fs[e] = static_cast<uint16_t>(key[r] & 0xffffu);
+        }
+        __syncwarp();
+    }
+
+    __device__ void sort_flush_rank(int nsel) {
+        // ps[np, np + nsel) is free scratch (np + nsel <= cap)
+        for (int i = lane; i < nsel; i += 32) {
+            const int si = w.fs[i];
+            const int64_t ti = pool_t(si);
+            int rank = 0;
+            for (int j = 0; j < nsel; ++j) {
+                const int64_t tj = pool_t(w.fs[j]);
+                rank += (tj < ti) || (tj == ti && j < i);
+            }
+            w.ps[np + rank] = static_cast<uint16_t>(si);
+        }
+        __syncwarp();
+        for (int i = lane; i < nsel; i += 32) w.fs[i] = w.ps[np + i];
+        __syncwarp();
+    }
+
+    // Finalise every pending knot with t < F (all of them if all_): select
+    // and sort them, merge equal positions, and turn each distinct position
+    // into a FieldPiece -- the running polynomial being the prefix sum of the
+    // jumps Taylor-shifted to a common origin tref (exact modulo 2^64, so
+    // equal to RayAccumulator's Int128 result whenever that fits int64).
+    __device__ void flush(int64_t F, bool all_) {
+        // ---- select t < F into fs, compact the rest of ps in place
+        int nsel = 0, nkeep = 0;
+        int64_t tmin = INT64_MAX, tmax = INT64_MIN;
+        for (int c0 = 0; c0 < np; c0 += 32) {
+            const int i = c0 + lane;
+            const bool valid = i < np;
+            const int s = valid ? w.ps[i] : 0;
+            const int64_t t = valid ? pool_t(s) : 0;
+            const bool sel = valid && (all_ || t < F);
+            const unsigned msel = __ballot_sync(kFull, sel);
+            const unsigned mkeep = __ballot_sync(kFull, valid && !sel);
+            __syncwarp();
+            if (sel) {
+                w.fs[nsel + __popc(msel & lanemask_lt())] = static_cast<uint16_t>(s);
+                tmin = t < tmin ? t : tmin;
+                tmax = t > tmax ? t : tmax;
+            } else if (valid) {
+                w.ps[nkeep + __popc(mkeep & lanemask_lt())] = static_cast<uint16_t>(s);
+            }
+            nsel += __popc(msel);
+            nkeep += __popc(mkeep);
+        }
+        __syncwarp();
+        np = nkeep;
+        if (nsel == 0) return;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int64_t a = __shfl_xor_sync(kFull, tmin, o);
+            const int64_t b = __shfl_xor_sync(kFull, tmax, o);
+            tmin = a < tmin ? a : tmin;
+            tmax = b > tmax ? b : tmax;
+        }
+        const bool packable = static_cast<uint64_t>(tmax) - static_cast<uint64_t>(tmin) < (1ull << 47);
+        if (packable && nsel <= 128)
+            sort_flush_reg<4>(nsel, tmin);
+        else if (packable && nsel <= 256)
+            sort_flush_reg<8>(nsel, tmin);
+        else if (packable && nsel <= 512)
+            sort_flush_reg<16>(nsel, tmin);
+        else
+            sort_flush_rank(nsel);
+
+        // ---- merge: 32 knots at a time
+        for (int c0 = 0; c0 < nsel; c0 += 32) {
+            const int i = c0 + lane;
+            const bool valid = i < nsel;
+            const int s = valid ? w.fs[i] : 0;
+            const int64_t t = valid ? pool_t(s) : 0;
+            const bool last = valid && ((i == nsel - 1) || (pool_t(w.fs[i + 1]) != t));
             if (!has_ref) {
                 tref = __shfl_sync(kFull, t, 0);
                 has_ref = true;
             }
             uint64_t g[D + 1];
-#pragma unroll
             g[0] = 0ull;  // b_0 == 0 for every knot
 #pragma unroll
-            for (int d = 1; d <= D; ++d) g[d] = valid ? w.pool[(d - 1) * P.cap + s] : 0ull;
+            for (int d = 1; d <= D; ++d) g[d] = valid ? pool_c(d, s) : 0ull;
             taylor_shift<D>(g, static_cast<uint64_t>(tref) - static_cast<uint64_t>(t));
 #pragma unroll
             for (int d = 0; d <= D; ++d) {
@@ -538,12 +549,12 @@ class RayWorker {
             const unsigned pm = __ballot_sync(kFull, last);
             const int cp = __popc(pm);
             if (last) {
+                // the piece at t: a = S(t - tref) G
                 taylor_shift<D>(g, static_cast<uint64_t>(t) - static_cast<uint64_t>(tref));
 #pragma unroll
-                for (int d = 1; d <= D; ++d) w.pool[(d - 1) * P.cap + s] = g[d];
+                for (int d = 1; d <= D; ++d) pool_c(d, s) = g[d];
                 const int pr = __popc(pm & lanemask_lt());
-                w.nt[pr] = t;
-                w.ns[pr] = static_cast<uint16_t>(s);
+                w.pcs[pr] = static_cast<uint16_t>(s);
                 w.na0[pr] = g[0];
                 if (P.dump_piece_t) {
                     const unsigned long long at = atomicAdd(&P.dump_count[1], 1ull);
@@ -560,24 +571,6 @@ class RayWorker {
             free_slots(valid && !last, s);
             if (cp > 0) composite_chunk(cp);
         }
-        // drop the flushed prefix
-        const int rest = np - nf;
-        for (int c0 = 0; c0 < rest; c0 += 32) {
-            const int i = c0 + lane;
-            int64_t t = 0;
-            uint16_t s = 0;
-            if (i < rest) {
-                t = w.pt[nf + i];
-                s = w.ps[nf + i];
-            }
-            __syncwarp();
-            if (i < rest) {
-                w.pt[i] = t;
-                w.ps[i] = s;
-            }
-            __syncwarp();
-        }
-        np = rest;
     }
 
     __device__ void report_overflow(int pi) {
@@ -585,10 +578,9 @@ class RayWorker {
         atomicMin(&P.stats[kStatOverflowKey], key);
     }
 
-    // Quantize the first nq queued hits (lane per hit) and merge their knots
-    // into the sorted window.  Returns false if the window is too small.
+    // Quantize the first nq queued hits (lane per hit) and append their knots
+    // to the pending list.  Returns false if the window is too small.
     __device__ bool insert_hits(int nq) {
-        constexpr int R = C::R;
         const bool act = lane < nq;
         int pi = 0;
         double lam = 0.0, tchi = 0.0, h = 0.0;
@@ -612,14 +604,6 @@ class RayWorker {
         if (total == 0) return true;
         if (total > nfree) return false;  // the caller flushed; the window is genuinely full
         const int slot0 = nfree - total + off;  // this lane's slots: fl[slot0 .. slot0 + nk)
-        int64_t kt[R];
-        int ks[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            kt[r] = INT64_MAX;
-            ks[r] = -1;  // padding marker
-        }
-        const bool odd = lane & 1;
         if (emits) {
             double X[2 * D];
             const double* xs = P.xy + static_cast<size_t>(pi) * (2 * D);
@@ -628,86 +612,15 @@ class RayWorker {
             quantize_emit<D, M>(P.Q, X, hp, ovf, [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
                 const int slot = w.fl[slot0 + o];
                 // b[0] is structurally zero (lut.hpp:107-166): only orders 1..D are stored
+                w.pool[slot] = static_cast<uint64_t>(t);
 #pragma unroll
-                for (int d = 1; d <= D; ++d) w.pool[(d - 1) * P.cap + slot] = static_cast<uint64_t>(b[d]);
-                const int at = odd ? R - 1 - o : o;  // odd lanes hold a descending block
-#pragma unroll
-                for (int r = 0; r < R; ++r)
-                    if (r == at) {
-                        kt[r] = t;
-                        ks[r] = slot;
-                    }
+                for (int d = 1; d <= D; ++d) pool_c(d, slot) = static_cast<uint64_t>(b[d]);
+                w.ps[np + off + o] = static_cast<uint16_t>(slot);
             });
             if (ovf) report_overflow(pi);
         }
         __syncwarp();
         nfree -= total;
-
-        // sort the new knots.  Packed keys when the batch spans < 2^47 tau
-        // (always, in practice); the (t, slot) pair network otherwise.
-        int64_t lo_t = emits ? hp.kpos[0] : INT64_MAX;
-        int64_t hi_t = emits ? hp.pos[M] : INT64_MIN;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const int64_t a = __shfl_xor_sync(kFull, lo_t, o);
-            const int64_t b = __shfl_xor_sync(kFull, hi_t, o);
-            lo_t = a < lo_t ? a : lo_t;
-            hi_t = b > hi_t ? b : hi_t;
-        }
-        if (static_cast<uint64_t>(hi_t) - static_cast<uint64_t>(lo_t) < (1ull << 47) && hi_t >= lo_t) {
-            uint64_t key[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-                key[r] = ks[r] < 0 ? ~0ull
-                                   : ((static_cast<uint64_t>(kt[r]) - static_cast<uint64_t>(lo_t)) << 16) |
-                                         static_cast<uint64_t>(ks[r]);
-            bitonic_sort_keys<R>(key, lane);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                kt[r] = static_cast<int64_t>(static_cast<uint64_t>(lo_t) + (key[r] >> 16));
-                ks[r] = static_cast<int>(key[r] & 0xffffu);
-            }
-        } else {
-            bitonic_sort<R>(kt, ks, lane);
-        }
-        int dB[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int e = lane * R + r;
-            dB[r] = 0;
-            if (e < total) {
-                w.nt[e] = kt[r];
-                w.ns[e] = static_cast<uint16_t>(ks[r]);
-                dB[r] = e + upper_bound64(w.pt, np, kt[r]);
-            }
-        }
-        __syncwarp();
-        for (int c0 = ((np - 1) / 32) * 32; np > 0 && c0 >= 0; c0 -= 32) {
-            const int i = c0 + lane;
-            int64_t t = 0;
-            uint16_t s = 0;
-            int dest = 0;
-            if (i < np) {
-                t = w.pt[i];
-                s = w.ps[i];
-                dest = i + lower_bound64(w.nt, total, t);
-            }
-            __syncwarp();
-            if (i < np) {
-                w.pt[dest] = t;
-                w.ps[dest] = s;
-            }
-            __syncwarp();
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int e = lane * R + r;
-            if (e < total) {
-                w.pt[dB[r]] = kt[r];
-                w.ps[dB[r]] = static_cast<uint16_t>(ks[r]);
-            }
-        }
-        __syncwarp();
         np += total;
         knots += total;
         if (np > max_pending) max_pending = np;
@@ -778,29 +691,36 @@ class RayWorker {
                 const uint32_t next = hq_n > 0 ? static_cast<uint32_t>(w.hq_c[0]) : cursor;
                 F = knot_floor(P.front[P.cand[next]], P.Q.tau);
             }
-            if (final_ || nfree < 32 * C::KN || lower_bound64(w.pt, np, F) >= 32) flush(F, final_);
+            if (final_ || nfree < 32 * KN || np >= (P.cap >> 1)) flush(F, final_);
             if (final_) break;
             if (term && P.mode == SPHRAY_MODE_FAST) break;
             if (hq_n > 0) {
-                const int nq = hq_n < 32 ? hq_n : 32;
-                if (!insert_hits(nq)) return false;
+                // as many queued hits as the window can surely take (each emits
+                // at most KN knots); none fitting after a flush = true overflow
+                const int fit = nfree / KN;
+                const int nq = min(min(hq_n, 32), fit);
+                if (nq == 0 || !insert_hits(nq)) return false;
+                // drop the nq inserted hits (up to 63 queued: shift in chunks)
                 const int rest = hq_n - nq;
-                int32_t qc = 0, qp = 0;
-                double ql = 0.0, qt = 0.0;
-                if (lane < rest) {
-                    qc = w.hq_c[nq + lane];
-                    qp = w.hq_p[nq + lane];
-                    ql = w.hq_lam[nq + lane];
-                    qt = w.hq_t[nq + lane];
+                for (int c0 = 0; c0 < rest; c0 += 32) {
+                    const int i = c0 + lane;
+                    int32_t qc = 0, qp = 0;
+                    double ql = 0.0, qt = 0.0;
+                    if (i < rest) {
+                        qc = w.hq_c[nq + i];
+                        qp = w.hq_p[nq + i];
+                        ql = w.hq_lam[nq + i];
+                        qt = w.hq_t[nq + i];
+                    }
+                    __syncwarp();
+                    if (i < rest) {
+                        w.hq_c[i] = qc;
+                        w.hq_p[i] = qp;
+                        w.hq_lam[i] = ql;
+                        w.hq_t[i] = qt;
+                    }
+                    __syncwarp();
                 }
-                __syncwarp();
-                if (lane < rest) {
-                    w.hq_c[lane] = qc;
-                    w.hq_p[lane] = qp;
-                    w.hq_lam[lane] = ql;
-                    w.hq_t[lane] = qt;
-                }
-                __syncwarp();
                 hq_n = rest;
             }
         }
@@ -824,7 +744,7 @@ class RayWorker {
             bool residual = false;  // raycast.hpp:477-480: trailing piece must be zero
             if (knots > 0 && complete && has_open) {
 #pragma unroll
-                for (int d = 1; d <= D; ++d) residual |= w.pool[(d - 1) * P.cap + open_slot] != 0;
+                for (int d = 1; d <= D; ++d) residual |= pool_c(d, open_slot) != 0;
                 residual |= open_a0 != 0;
             }
             // RayAccumulator op count for P distinct positions (raycast.hpp:217-244)
@@ -849,7 +769,7 @@ __global__ void __maxnreg__(168) k_render_rays(const FrameParams P) {
     extern __shared__ __align__(16) char smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const WarpMem wm = carve(smem + static_cast<size_t>(warp) * P.warp_bytes, D, P.cap, Cfg<M>::NB);
+    const WarpMem wm = carve(smem + static_cast<size_t>(warp) * P.warp_bytes, D, P.cap);
     RayWorker<D, M> rw(P, wm, lane);
     while (true) {
         unsigned long long item = 0;
@@ -916,7 +836,6 @@ __global__ void k_quantize_hits(const QuantParams Q, const sphray_particle* ps, 
     });
     knot_count[i] = ovf ? -1 : hp.nk;
 }
-
 
 }  // namespace rk
 

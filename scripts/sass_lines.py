@@ -18,13 +18,15 @@ def main():
     own = ("render_kernel.cuh", "quantize.cuh", "device_math.cuh", "render.cu")
     i0 = next(i for i, l in enumerate(txt) if l.startswith(".text.") and kern in l)
     cur, off2line, static = None, {}, Counter()
-    chain = []
+    chain, fresh = [], True
     for l in txt[i0 + 1:]:
         if l.startswith(".text.") or l.strip().startswith(".section"):
             if off2line:
                 break
         m = re.search(r'//## File "([^"]+)", line (\d+)(?: inlined at "([^"]+)", line (\d+))?', l)
         if m:
+            if fresh:
+                chain, fresh = [], False
             chain.append((m.group(1).split("/")[-1], int(m.group(2))))
             if m.group(3):
                 chain.append((m.group(3).split("/")[-1], int(m.group(4))))
@@ -37,7 +39,7 @@ def main():
                 cur = chain[0]
             continue
         if re.search(r"/\*[0-9a-f]{4,}\*/", l):
-            chain = []
+            fresh = True
         m = re.search(r"/\*([0-9a-f]{4,})\*/\s+(\S+)", l)
         if m and cur:
             off = int(m.group(1), 16)
