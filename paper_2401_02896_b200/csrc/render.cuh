@@ -33,6 +33,7 @@ SPHRAY_HD inline size_t warp_bytes_for(int D, int cap) {
     b += align16(sizeof(int32_t) * kHitQueue * 2);
     b += align16(sizeof(uint16_t) * cap * 3);         // ps, fl, fs
     b += align16(sizeof(uint16_t) * 32);              // pcs
+    b += align16(sizeof(uint32_t) * 256);             // radix bins
     return b;
 }
 
