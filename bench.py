@@ -230,7 +230,8 @@ def run_ours(args):
     SD.init_comm(ctx, rank, world)
     cam = S.Camera(**camera_kwargs(res))
     tf = S.TransferFunction.from_array(SYNTH_TF)
-    opts = S.RenderOptions(mode=S.MODE_FAST if args.mode == "fast" else S.MODE_EXACT)
+    opts = S.RenderOptions(mode=S.MODE_FAST if args.mode == "fast" else S.MODE_EXACT,
+                           window=args.window)
     ctx.upload(ps, lut)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr())
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -369,6 +370,7 @@ def main():
     ap.add_argument("--res", type=int, default=0, help="override image resolution (profiling)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--window", type=int, default=0, help="knot window slots per ray (0 = auto)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-step-budget", type=float, default=5.0)

@@ -19,6 +19,10 @@
 #include "quantize.cuh"
 #include "render.cuh"
 
+#ifndef SPHRAY_MAXNREG
+#define SPHRAY_MAXNREG 168
+#endif
+
 namespace sphray_b200 {
 namespace rk {
 
@@ -256,34 +260,55 @@ class RayWorker {
     }
 
     // Samples of one piece, front to back, from transmittance T0 (composite(),
-    // raycast.hpp:369-377): midpoint t = lo + (s + 0.5) dt exactly as the
-    // reference places them; the piece polynomial (evaluate_piece,
-    // raycast.hpp:295-301) in fp64 Horner; alpha = 1 - exp(-absorption dt)
-    // through fp32 expm1 (relative error ~1e-7, inside the stated 1e-4 RGB
-    // tolerance); colour and transmittance accumulate in fp64.  With `stop`
-    // the reference's T > 1e-3 check runs before every sample.
-    __device__ __forceinline__ void sample_piece(const double (&c)[D + 1], int64_t ts, double lo,
+    // raycast.hpp:369-377): midpoints lo + (s + 1/2) dt as the reference
+    // places them, taken here as the piece-local abscissa x = x0 + (s + 1/2) dx
+    // (x0 = lo/tau - t_piece, dx = dt/tau; evaluate_piece, raycast.hpp:295-301)
+    // and fp64 Horner on sigma-scaled coefficients; alpha = 1 - exp(-ab dt)
+    // via alpha_of; colour and transmittance accumulate in fp64.  Two samples
+    // are evaluated per iteration (independent until the transmittance
+    // update) for ILP.  With `stop` the reference's T > 1e-3 check runs before
+    // every sample (the early-termination replay).
+    __device__ __forceinline__ void sample_eval(const double (&c)[D + 1], double x, double dt,
+                                                double& alpha, double& r, double& g,
+                                                double& b) const {
+        double acc = c[D];
+#pragma unroll
+        for (int d = D - 1; d >= 0; --d) acc = fma(acc, x, c[d]);
+        double ab;
+        tf_sample(P.tf, P.ntf, acc, r, g, b, ab);
+        alpha = alpha_of(ab * dt);
+    }
+
+    __device__ __forceinline__ void sample_piece(const double (&c)[D + 1], double x0, double dx,
                                                  double dt, int n, double T0, bool stop,
                                                  double& Tout, double& cr, double& cg,
                                                  double& cb) const {
         Tout = T0;
         cr = cg = cb = 0.0;
-        const double tsd = static_cast<double>(ts);
-        for (int s = 0; s < n; ++s) {
+        int s = 0;
+        if (!stop) {
+            for (; s + 1 < n; s += 2) {
+                double a0, r0, g0, b0, a1, r1, g1, b1;
+                sample_eval(c, fma(static_cast<double>(s) + 0.5, dx, x0), dt, a0, r0, g0, b0);
+                sample_eval(c, fma(static_cast<double>(s) + 1.5, dx, x0), dt, a1, r1, g1, b1);
+                const double ta0 = Tout * a0;
+                const double T1 = Tout * (1.0 - a0);
+                const double ta1 = T1 * a1;
+                cr = fma(ta1, r1, fma(ta0, r0, cr));
+                cg = fma(ta1, g1, fma(ta0, g0, cg));
+                cb = fma(ta1, b1, fma(ta0, b0, cb));
+                Tout = T1 * (1.0 - a1);
+            }
+        }
+        for (; s < n; ++s) {
             if (stop && !(Tout > 1e-3)) break;
-            const double t = dadd(lo, dmul(dadd(static_cast<double>(s), 0.5), dt));
-            const double x = t * P.inv_tau - tsd;
-            double acc = c[D];
-#pragma unroll
-            for (int d = D - 1; d >= 0; --d) acc = fma(acc, x, c[d]);
-            double r, g, b, ab;
-            tf_sample(P.tf, P.ntf, acc * P.Q.sigma, r, g, b, ab);
-            const double alpha = alpha_of(ab * dt);
-            const double ta = Tout * alpha;
+            double a, r, g, b;
+            sample_eval(c, fma(static_cast<double>(s) + 0.5, dx, x0), dt, a, r, g, b);
+            const double ta = Tout * a;
             cr = fma(ta, r, cr);
             cg = fma(ta, g, cg);
             cb = fma(ta, b, cb);
-            Tout = Tout * (1.0 - alpha);
+            Tout = Tout * (1.0 - a);
         }
     }
 
@@ -309,7 +334,7 @@ class RayWorker {
 
         if (!term) {
             int n = 0;
-            double lo = 0.0, dt = 0.0;
+            double lo = 0.0, dt = 0.0, x0 = 0.0, dx = 0.0;
             double c[D + 1];
 #pragma unroll
             for (int d = 0; d <= D; ++d) c[d] = 0.0;
@@ -324,13 +349,15 @@ class RayWorker {
                     n = sample_count(len, P.step, P.inv_step);
                     dt = n <= kLaneSamples ? len * c_inv_small[n] : len / static_cast<double>(n);
                     bool zero = a0 == 0;
-                    c[0] = static_cast<double>(static_cast<int64_t>(a0));
+                    c[0] = static_cast<double>(static_cast<int64_t>(a0)) * P.Q.sigma;
 #pragma unroll
                     for (int d = 1; d <= D; ++d) {
                         const int64_t a = static_cast<int64_t>(pool_c(d, slot));
                         zero &= a == 0;
-                        c[d] = static_cast<double>(a);
+                        c[d] = static_cast<double>(a) * P.Q.sigma;
                     }
+                    x0 = fma(lo, P.inv_tau, -static_cast<double>(ts));
+                    dx = dt * P.inv_tau;
                     // alpha = 1 - exp(-0) = 0 exactly: no colour, T unchanged
                     if (zero && P.tf0_clear) n = 0;
                 }
@@ -338,7 +365,7 @@ class RayWorker {
             const int maxn = __reduce_max_sync(kFull, n);
             if (maxn > 0 && maxn <= kLaneSamples) {
                 double Tl, cr, cg, cb;
-                sample_piece(c, ts, lo, dt, n, 1.0, false, Tl, cr, cg, cb);
+                sample_piece(c, x0, dx, dt, n, 1.0, false, Tl, cr, cg, cb);
                 // exclusive prefix product of the lanes' transmittances
                 double pre = Tl;
 #pragma unroll
@@ -360,7 +387,7 @@ class RayWorker {
                 if (f < 32) {
                     double Tr = 0.0, r2 = 0.0, g2 = 0.0, b2 = 0.0;
                     if (lane == f) {
-                        sample_piece(c, ts, lo, dt, n, Tb, true, Tr, r2, g2, b2);
+                        sample_piece(c, x0, dx, dt, n, Tb, true, Tr, r2, g2, b2);
                         rr = r2;
                         gg = g2;
                         bb = b2;
@@ -373,7 +400,7 @@ class RayWorker {
                 Cb += warp_sum(bb);
                 T = Tend;
             } else if (maxn > 0) {
-                composite_balanced(n, lo, dt, ts, c);
+                composite_balanced(n, x0, dx, dt, c);
             }
         }
         // composited start pieces are dead: their slots return to the pool
@@ -385,7 +412,7 @@ class RayWorker {
 
     // Sample-parallel compositing for chunks containing long pieces: samples
     // are dealt 32 at a time across the lanes, in order.
-    __device__ void composite_balanced(int n, double lo, double dt, int64_t ts,
+    __device__ void composite_balanced(int n, double x0, double dx, double dt,
                                        const double (&cl)[D + 1]) {
         const int incl = warp_incl_scan(n, lane);
         const int total = __shfl_sync(kFull, incl, 31);
@@ -404,23 +431,14 @@ class RayWorker {
             }
             const int j = lo_l;
             const int s = k - (__shfl_sync(kFull, incl, j) - __shfl_sync(kFull, n, j));
-            const double lo_j = __shfl_sync(kFull, lo, j);
+            const double x0_j = __shfl_sync(kFull, x0, j);
+            const double dx_j = __shfl_sync(kFull, dx, j);
             const double dt_j = __shfl_sync(kFull, dt, j);
-            const int64_t ts_j = __shfl_sync(kFull, ts, j);
             double c[D + 1];
 #pragma unroll
             for (int d = 0; d <= D; ++d) c[d] = __shfl_sync(kFull, cl[d], j);
             double alpha = 0.0, r = 0.0, g = 0.0, b = 0.0;
-            if (act) {
-                const double t = dadd(lo_j, dmul(dadd(static_cast<double>(s), 0.5), dt_j));
-                const double x = t * P.inv_tau - static_cast<double>(ts_j);
-                double acc = c[D];
-#pragma unroll
-                for (int d = D - 1; d >= 0; --d) acc = fma(acc, x, c[d]);
-                double ab;
-                tf_sample(P.tf, P.ntf, acc * P.Q.sigma, r, g, b, ab);
-                alpha = alpha_of(ab * dt_j);
-            }
+            if (act) sample_eval(c, fma(static_cast<double>(s) + 0.5, dx_j, x0_j), dt_j, alpha, r, g, b);
             const double f = act ? 1.0 - alpha : 1.0;
             double pre = f;
 #pragma unroll
@@ -452,9 +470,11 @@ class RayWorker {
     __device__ void sort_flush_radix(int nsel, int64_t tmin, int bits) {
         uint16_t* src = w.fs;
         uint16_t* dst = w.ps + np;  // free scratch: np + nsel <= cap
+#pragma unroll 1
         for (int shift = 0; shift < bits; shift += 8) {
             for (int i = lane; i < 256; i += 32) w.hist[i] = 0;
             __syncwarp();
+#pragma unroll 1
             for (int i = lane; i < nsel; i += 32) {
                 const uint32_t dg = static_cast<uint32_t>(
                     ((static_cast<uint64_t>(pool_t(src[i])) - static_cast<uint64_t>(tmin)) >> shift) & 255u);
@@ -473,6 +493,7 @@ class RayWorker {
 #pragma unroll
             for (int k = 0; k < 8; ++k) w.hist[lane * 8 + k] = before + loc[k];
             __syncwarp();
+#pragma unroll 1
             for (int c0 = 0; c0 < nsel; c0 += 32) {
                 const int i = c0 + lane;
                 const bool valid = i < nsel;
@@ -802,7 +823,7 @@ class RayWorker {
 };
 
 template <int D, int M>
-__global__ void __maxnreg__(168) k_render_rays(const FrameParams P) {
+__global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const FrameParams P) {
     extern __shared__ __align__(16) char smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;

@@ -34,7 +34,7 @@ def main():
             if mine:
                 inner = mine[0]
                 caller = next((c for c in mine[1:] if c != inner), None)
-                cur = (inner[0], inner[1] if caller is None else f"{inner[1]}<{caller[1]}")
+                cur = (inner[0], inner[1] if caller is None else f"{inner[1]}<{caller[0][:6]}:{caller[1]}")
             else:
                 cur = chain[0]
             continue
@@ -65,7 +65,7 @@ def main():
     print(f"static SASS instructions: {tot_s}")
     key = dyn if dyn else static
     for ln, _ in key.most_common(45):
-        print(f"{ln[0]}:{str(ln[1]):>10s}  static {static[ln]:5d}  exec {dyn[ln]/tot_d*100:5.1f}%  stall {stall[ln]/tot_st*100:5.1f}%")
+        print(f"{ln[0]}:{str(ln[1]):>18s}  static {static[ln]:5d}  exec {dyn[ln]/tot_d*100:5.1f}%  stall {stall[ln]/tot_st*100:5.1f}%")
 
 
 if __name__ == "__main__":
