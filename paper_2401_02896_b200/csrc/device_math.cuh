@@ -155,8 +155,18 @@ __device__ __forceinline__ double front_bound(const CamConst& c, double x, doubl
 
 // Lut::lookup (lut.hpp:43-52) for lam < q (quantize_particle returns before
 // the zero entry: quantize.hpp:204).
-__device__ __forceinline__ int lut_index(double lam, double dl, int N) {
-    const double x = ddiv(lam, dl);
+static __device__ __noinline__ double div_exact(double a, double b) { return ddiv(a, b); }
+
+// inv_dl = recip_or_nan(dl): x = lam/dl is taken as lam*inv_dl when that is
+// farther than |x| 2^-50 from every integer (then floor and the tie test
+// agree with the correctly rounded quotient), else divided exactly.
+__device__ __forceinline__ int lut_index(double lam, double dl, double inv_dl, int N) {
+    double x = lam * inv_dl;
+    {
+        const double f = floor(x);
+        const double mg = fabs(x) * 0x1p-50;
+        if (!(x - f > mg && (f + 1.0) - x > mg && fabs(x) < 0x1p49)) x = div_exact(lam, dl);
+    }
     double i = floor(x);
     if (i == x && i > 0.0) i = dsub(i, 1.0);
     const double c = (i < 0.0) ? 0.0 : i;
@@ -195,6 +205,40 @@ __device__ __forceinline__ int64_t round_checked(double x, bool& o) {
     const bool ok = r >= -9223372036854775808.0 && r < 9223372036854775808.0;
     o |= !ok;
     return ok ? __double2ll_rn(r) : 0;
+}
+
+// Correctly rounded reciprocal for the division fast paths below, or NaN
+// (forcing the exact path) when it is not a normal number.
+__host__ __device__ inline double recip_or_nan(double b) {
+    const double y = 1.0 / b;
+    const double ay = y < 0.0 ? -y : y;
+    return (ay >= 0x1p-1000 && ay <= 0x1p1000) ? y : __builtin_nan("");
+}
+
+struct RintQ {
+    int64_t v;
+    bool ovf;
+};
+// Exact path, out of line: one copy of the division code for every call site.
+static __device__ __noinline__ RintQ rint_div_exact(double a, double b) {
+    bool o = false;
+    const int64_t v = round_checked(ddiv(a, b), o);
+    return {v, o};
+}
+
+// round_to_int(a / b) with the quotient correctly rounded as the reference
+// computes it, from y = recip_or_nan(b).  q = a*y is within |q| 2^-51 of
+// RN(a/b) (two roundings of relative size 2^-53); when q is farther than
+// |q| 2^-50 from every half-integer, rint(q) == rint(RN(a/b)).  Otherwise
+// (and for |q| >= 2^49, NaN, inf) the exact division decides.
+__device__ __forceinline__ int64_t rint_div(double a, double b, double y, bool& o) {
+    const double q = a * y;
+    const double r = rint(q);
+    const double aq = fabs(q);
+    if (aq < 0x1p49 && fabs(q - r) < 0.5 - aq * 0x1p-50) return static_cast<int64_t>(r);
+    const RintQ e = rint_div_exact(a, b);
+    o |= e.ovf;
+    return e.v;
 }
 
 // Taylor shift p(y) -> p(y + delta) modulo 2^64 (repeated Horner).  This is

@@ -251,6 +251,13 @@ constexpr size_t kSmemLimit = 227 * 1024;
 }  // namespace
 
 namespace {
+// host twin of dev::recip_or_nan (device_math.cuh)
+double recip_or_nan(double b) {
+    const double y = 1.0 / b;
+    const double ay = std::fabs(y);
+    return (ay >= 0x1p-1000 && ay <= 0x1p1000) ? y : std::numeric_limits<double>::quiet_NaN();
+}
+
 // SPHRAY_TRACE=1: host-side phase timings of each frame on stderr
 struct Trace {
     bool on = std::getenv("SPHRAY_TRACE") != nullptr;
@@ -324,7 +331,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     if (n > 0) {
         d_bbox_.ensure(static_cast<size_t>(n) * sizeof(int4));
         d_front_.ensure(static_cast<size_t>(n) * sizeof(float));
-        d_xy_.ensure(static_cast<size_t>(n) * 2 * D * sizeof(double));
+        d_xy_.ensure(static_cast<size_t>(n) * 3 * D * sizeof(double));
         d_counts_.ensure(static_cast<size_t>(n) * 4);
         d_offsets_.ensure(static_cast<size_t>(n) * 4);
         PrepParams pp{};
@@ -409,6 +416,8 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     P.Q.m = lut_.m;
     P.Q.tau = qc.tau;
     P.Q.sigma = qc.sigma;
+    P.Q.inv_tau = recip_or_nan(qc.tau);
+    P.Q.inv_dl = recip_or_nan(lut_.delta_lambda);
     P.n = n;
     P.pxyzh = d_pxyzh_.as<double4>();
     P.xy = d_xy_.as<double>();
@@ -568,6 +577,12 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         CUDA_OK(cudaStreamSynchronize(s));
     }
     trace.mark("tail");
+    if (trace.on && (st[kStatFlushes] | st[kStatBatches])) {
+        static const char* names[] = {"flushes", "scanned", "selected", "chunks", "radix_passes",
+                                      "batches", "samples", "balanced", "gather"};
+        for (int k = kStatFirstK; k < kStatCount; ++k)
+            trace.line += std::string(" ") + names[k - kStatFirstK] + "=" + std::to_string(st[k]);
+    }
     float ms = 0.0f, ms_bin = 0.0f, ms_render = 0.0f;
     CUDA_OK(cudaEventElapsedTime(&ms, ev0_, ev1_));
     CUDA_OK(cudaEventElapsedTime(&ms_bin, ev0_, evr0_));
@@ -678,6 +693,8 @@ void Engine::quantize_hits(const sphray_particle* ps, size_t nhits, const double
     Q.m = L.m;
     Q.tau = qc.tau;
     Q.sigma = qc.sigma;
+    Q.inv_tau = recip_or_nan(qc.tau);
+    Q.inv_dl = recip_or_nan(L.delta_lambda);
     launch_quantize_hits(Q, D, dps.as<sphray_particle>(), dpw.as<double>(), dpt.as<double>(), nhits,
                          dtc.as<double>(), dla.as<double>(), dkt.as<int64_t>(), dkb.as<int64_t>(),
                          dkc.as<int32_t>(), stream_);

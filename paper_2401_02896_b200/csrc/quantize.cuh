@@ -12,10 +12,19 @@
 namespace sphray_b200 {
 namespace dev {
 
-__constant__ long long c_binom[7][7] = {{1, 0, 0, 0, 0, 0, 0},  {1, 1, 0, 0, 0, 0, 0},
-                                        {1, 2, 1, 0, 0, 0, 0},  {1, 3, 3, 1, 0, 0, 0},
-                                        {1, 4, 6, 4, 1, 0, 0},  {1, 5, 10, 10, 5, 1, 0},
-                                        {1, 6, 15, 20, 15, 6, 1}};
+constexpr long long binom(int n, int k) {
+    long long r = 1;
+    for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+    return r;
+}
+
+// Checked multiply by a binomial c > 0 (Checked<int64_t> *); c is a
+// constant after unrolling, so the bounds fold and c == 1 costs nothing.
+__device__ __forceinline__ int64_t cmul_binom(int64_t a, long long c, bool& o) {
+    if (c == 1) return a;
+    o |= a > INT64_MAX / c || a < INT64_MIN / c;
+    return static_cast<int64_t>(static_cast<uint64_t>(a) * static_cast<uint64_t>(c));
+}
 
 template <int M>
 struct HitPositions {
@@ -44,12 +53,12 @@ __device__ __forceinline__ bool quantize_positions(const QuantParams& Q, double 
 #pragma unroll
     for (int q = 0; q < KN; ++q) hp.kpos[q] = 0;
     if (!(lam < Q.q)) return false;
-    const int e = lut_index(lam, Q.lut_dl, Q.lut_N);
+    const int e = lut_index(lam, Q.lut_dl, Q.inv_dl, Q.lut_N);
     hp.row = Q.lut_rows + static_cast<size_t>(e) * Q.lut_stride;
-    hp.pos[0] = round_checked(ddiv(tchi, Q.tau), ovf);
+    hp.pos[0] = rint_div(tchi, Q.tau, Q.inv_tau, ovf);
 #pragma unroll
     for (int k = 1; k <= M; ++k)
-        hp.pos[k] = cadd(hp.pos[0], round_checked(ddiv(dmul(h, hp.row[k - 1]), Q.tau), ovf), ovf);
+        hp.pos[k] = cadd(hp.pos[0], rint_div(dmul(h, hp.row[k - 1]), Q.tau, Q.inv_tau, ovf), ovf);
     const int64_t twice = cadd(hp.pos[0], hp.pos[0], ovf);
     bool ov2 = false;  // the negative side is evaluated for all k; flags count once
 #pragma unroll
@@ -70,7 +79,8 @@ __device__ __forceinline__ bool quantize_positions(const QuantParams& Q, double 
 }
 
 // Phase B.  X[0..D) = (pow(tau,d)*mass)*value, X[D..2D) = (sigma*density)*pow(h,d+3)
-// (quantize.hpp:221-222 with the libm parts precomputed on the host).
+// (quantize.hpp:221-222 with the libm parts precomputed on the host),
+// X[2D..3D) = recip_or_nan(X[D..2D)) for rint_div.
 // sink(o, t, b) receives distinct knot o (0..nk) with its D+1 jumps.
 template <int D, int M, class Sink>
 __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double* X,
@@ -99,8 +109,7 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
             } else {
                 ii = c1 + (k - 2) * D + (d - 1);
             }
-            const double raw = ddiv(dmul(X[d - 1], hp.row[m + ii]), X[D + d - 1]);
-            const int64_t bp = round_checked(raw, ovf);
+            const int64_t bp = rint_div(dmul(X[d - 1], hp.row[m + ii]), X[D + d - 1], X[2 * D + d - 1], ovf);
             negk[k - 1][d] = (d & 1) ? bp : cneg(bp, ovf);  // lut.hpp:107-109
         }
     }
@@ -112,11 +121,13 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
 #pragma unroll
             for (int k = 1; k <= M; ++k) {
                 const int64_t off = csub(hp.pos[k], hp.pos[0], ovf);
-                int64_t pw = 1;
+                int64_t pw = 1;  // off^(j-d), built one step at a time as lut.hpp:123-126
 #pragma unroll
                 for (int j = d; j <= D; ++j) {
-                    acc = cadd(acc, cmul(cmul(c_binom[j][d], negk[k - 1][j], ovf), pw, ovf), ovf);
-                    if (j < D) pw = cmul(pw, off, ovf);
+                    int64_t t = cmul_binom(negk[k - 1][j], binom(j, d), ovf);
+                    if (j > d) t = cmul(t, pw, ovf);  // * 1 at j == d
+                    acc = cadd(acc, t, ovf);
+                    if (j < D) pw = (j == d) ? off : cmul(pw, off, ovf);
                 }
             }
             center[d] = cneg(cadd(acc, acc, ovf), ovf);
@@ -134,7 +145,7 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
                 int64_t pw = off;
 #pragma unroll
                 for (int j = d + 1; j <= D; ++j) {
-                    acc = cadd(acc, cmul(cmul(c_binom[j][d], negk[k - 1][j], ovf), pw, ovf), ovf);
+                    acc = cadd(acc, cmul(cmul_binom(negk[k - 1][j], binom(j, d), ovf), pw, ovf), ovf);
                     if (j < D) pw = cmul(pw, off, ovf);
                 }
             }

@@ -55,10 +55,12 @@ __global__ void k_prep(const PrepParams p) {
     p.counts[i] = cnt;
     // X_d = (pow(tau,d)*mass)*value, Y_d = (sigma*density)*pow(h,d+3)   (quantize.hpp:221-222)
     const double4 m = p.mvr[i];
-    double* xy = p.xy + static_cast<size_t>(i) * 2 * p.D;
+    double* xy = p.xy + static_cast<size_t>(i) * 3 * p.D;
     for (int d = 1; d <= p.D; ++d) {
         xy[d - 1] = dmul(dmul(p.powtau[d - 1], m.x), m.y);
-        xy[p.D + d - 1] = dmul(dmul(p.sigma, m.z), p.powh[static_cast<size_t>(i) * p.D + d - 1]);
+        const double y = dmul(dmul(p.sigma, m.z), p.powh[static_cast<size_t>(i) * p.D + d - 1]);
+        xy[p.D + d - 1] = y;
+        xy[2 * p.D + d - 1] = recip_or_nan(y);
     }
 }
 

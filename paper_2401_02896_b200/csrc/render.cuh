@@ -44,6 +44,7 @@ struct QuantParams {
     double lut_dl, q;
     int K, m;
     double tau, sigma;
+    double inv_tau, inv_dl;  // recip_or_nan(tau), recip_or_nan(lut_dl): division fast paths
 };
 
 // Per-frame constants of the render kernel.
@@ -53,7 +54,7 @@ struct FrameParams {
     // scene (Morton-ordered SoA)
     int n;
     const double4* pxyzh;  // x, y, z, h
-    const double* xy;      // n * 2D: X_1..X_D, Y_1..Y_D   (quantize.hpp:221-222)
+    const double* xy;      // n * 3D: X_1..X_D, Y_1..Y_D (quantize.hpp:221-222), 1/Y_1..1/Y_D
     const int4* bbox;      // reference footprint bbox per particle (clipped)
     const float* front;    // knot-position lower bound (world units, rounded down)
     const int32_t* orig;   // original particle index
@@ -106,8 +107,19 @@ enum StatIndex {
     kStatMaxPending = 5,
     kStatOverflowKey = 6,
     kStatSkipped = 7,
-    kStatCount = 8
+    // work counters, filled only in -DSPHRAY_KSTATS=1 builds (diagnostics)
+    kStatFlushes = 8,
+    kStatScanned = 9,   // pending entries examined by flush selection
+    kStatSelected = 10,  // knots finalised
+    kStatChunks = 11,    // 32-knot merge chunks
+    kStatRadixPasses = 12,
+    kStatBatches = 13,   // insert_hits calls
+    kStatSamples = 14,   // composited samples (lane path + balanced path)
+    kStatBalanced = 15,  // chunks sent to the sample-parallel path
+    kStatGather = 16,    // 32-candidate gather iterations
+    kStatCount = 17
 };
+constexpr int kStatFirstK = kStatFlushes;
 
 // Per-frame particle prep (view + quanta dependent).
 struct PrepParams {

@@ -19,6 +19,15 @@
 #include "quantize.cuh"
 #include "render.cuh"
 
+#ifndef SPHRAY_KSTATS
+#define SPHRAY_KSTATS 0
+#endif
+// diagnostic work counters (render.cuh StatIndex), compiled out by default
+#define SPHRAY_KS(idx, v)                                                            \
+    do {                                                                             \
+        if (SPHRAY_KSTATS && lane == 0)                                              \
+            atomicAdd(&P.stats[idx], static_cast<unsigned long long>(v));            \
+    } while (0)
 #ifndef SPHRAY_MAXNREG
 #define SPHRAY_MAXNREG 168
 #endif
@@ -219,7 +228,8 @@ class RayWorker {
     int open_slot = 0;     // last piece: its successor is not known yet
     uint64_t open_a0 = 0;  // its order-0 coefficient (the slot holds orders 1..D)
     bool has_open = false;
-    double T = 1.0, Cr = 0.0, Cg = 0.0, Cb = 0.0;
+    double T = 1.0;
+    double Cr = 0.0, Cg = 0.0, Cb = 0.0;  // per-lane partial colour sums (reduced in finish)
     bool term = false;
     unsigned long long knots = 0, pieces = 0, hits = 0;
     int max_pending = 0;
@@ -264,10 +274,10 @@ class RayWorker {
     // places them, taken here as the piece-local abscissa x = x0 + (s + 1/2) dx
     // (x0 = lo/tau - t_piece, dx = dt/tau; evaluate_piece, raycast.hpp:295-301)
     // and fp64 Horner on sigma-scaled coefficients; alpha = 1 - exp(-ab dt)
-    // via alpha_of; colour and transmittance accumulate in fp64.  Two samples
-    // are evaluated per iteration (independent until the transmittance
-    // update) for ILP.  With `stop` the reference's T > 1e-3 check runs before
-    // every sample (the early-termination replay).
+    // via alpha_of; colour and transmittance accumulate in fp64.  With `stop`
+    // the reference's T > 1e-3 check runs before every sample (the
+    // early-termination replay).  (Evaluating two samples per iteration for
+    // ILP measured 7% slower on config 3: more registers, longer code.)
     __device__ __forceinline__ void sample_eval(const double (&c)[D + 1], double x, double dt,
                                                 double& alpha, double& r, double& g,
                                                 double& b) const {
@@ -285,22 +295,7 @@ class RayWorker {
                                                  double& cb) const {
         Tout = T0;
         cr = cg = cb = 0.0;
-        int s = 0;
-        if (!stop) {
-            for (; s + 1 < n; s += 2) {
-                double a0, r0, g0, b0, a1, r1, g1, b1;
-                sample_eval(c, fma(static_cast<double>(s) + 0.5, dx, x0), dt, a0, r0, g0, b0);
-                sample_eval(c, fma(static_cast<double>(s) + 1.5, dx, x0), dt, a1, r1, g1, b1);
-                const double ta0 = Tout * a0;
-                const double T1 = Tout * (1.0 - a0);
-                const double ta1 = T1 * a1;
-                cr = fma(ta1, r1, fma(ta0, r0, cr));
-                cg = fma(ta1, g1, fma(ta0, g0, cg));
-                cb = fma(ta1, b1, fma(ta0, b0, cb));
-                Tout = T1 * (1.0 - a1);
-            }
-        }
-        for (; s < n; ++s) {
+        for (int s = 0; s < n; ++s) {
             if (stop && !(Tout > 1e-3)) break;
             double a, r, g, b;
             sample_eval(c, fma(static_cast<double>(s) + 0.5, dx, x0), dt, a, r, g, b);
@@ -363,6 +358,11 @@ class RayWorker {
                 }
             }
             const int maxn = __reduce_max_sync(kFull, n);
+            if (SPHRAY_KSTATS) {
+                const unsigned ns = __reduce_add_sync(kFull, static_cast<unsigned>(n));
+                SPHRAY_KS(kStatSamples, ns);
+            }
+            if (maxn > kLaneSamples) SPHRAY_KS(kStatBalanced, 1);
             if (maxn > 0 && maxn <= kLaneSamples) {
                 double Tl, cr, cg, cb;
                 sample_piece(c, x0, dx, dt, n, 1.0, false, Tl, cr, cg, cb);
@@ -395,9 +395,9 @@ class RayWorker {
                     Tend = __shfl_sync(kFull, Tr, f);
                     term = true;
                 }
-                Cr += warp_sum(rr);
-                Cg += warp_sum(gg);
-                Cb += warp_sum(bb);
+                Cr += rr;
+                Cg += gg;
+                Cb += bb;
                 T = Tend;
             } else if (maxn > 0) {
                 composite_balanced(n, x0, dx, dt, c);
@@ -455,9 +455,11 @@ class RayWorker {
             const int first_fail = fail ? __ffs(fail) - 1 : 32;
             const bool inc = act && lane < first_fail;
             const double ta = inc ? Tb * alpha : 0.0;
-            Cr += warp_sum(inc ? ta * r : 0.0);
-            Cg += warp_sum(inc ? ta * g : 0.0);
-            Cb += warp_sum(inc ? ta * b : 0.0);
+            if (inc) {
+                Cr = fma(ta, r, Cr);
+                Cg = fma(ta, g, Cg);
+                Cb = fma(ta, b, Cb);
+            }
             const unsigned incm = __ballot_sync(kFull, inc);
             if (incm) T = __shfl_sync(kFull, Tb * f, 31 - __clz(incm));
             if (fail) term = true;
@@ -472,6 +474,7 @@ class RayWorker {
         uint16_t* dst = w.ps + np;  // free scratch: np + nsel <= cap
 #pragma unroll 1
         for (int shift = 0; shift < bits; shift += 8) {
+            SPHRAY_KS(kStatRadixPasses, 1);
             for (int i = lane; i < 256; i += 32) w.hist[i] = 0;
             __syncwarp();
 #pragma unroll 1
@@ -567,6 +570,10 @@ class RayWorker {
             nkeep += __popc(mkeep);
         }
         __syncwarp();
+        SPHRAY_KS(kStatFlushes, 1);
+        SPHRAY_KS(kStatScanned, np);
+        SPHRAY_KS(kStatSelected, nsel);
+        SPHRAY_KS(kStatChunks, (nsel + 31) / 32);
         np = nkeep;
         if (nsel == 0) return;
 #pragma unroll
@@ -659,14 +666,15 @@ class RayWorker {
         }
         const int off = warp_incl_scan(nk, lane) - nk;
         const int total = __shfl_sync(kFull, off + nk, 31);
+        SPHRAY_KS(kStatBatches, 1);
         if (total == 0) return true;
         if (total > nfree) return false;  // the caller flushed; the window is genuinely full
         const int slot0 = nfree - total + off;  // this lane's slots: fl[slot0 .. slot0 + nk)
         if (emits) {
-            double X[2 * D];
-            const double* xs = P.xy + static_cast<size_t>(pi) * (2 * D);
+            double X[3 * D];
+            const double* xs = P.xy + static_cast<size_t>(pi) * (3 * D);
 #pragma unroll
-            for (int d = 0; d < 2 * D; ++d) X[d] = xs[d];
+            for (int d = 0; d < 3 * D; ++d) X[d] = xs[d];
             quantize_emit<D, M>(P.Q, X, hp, ovf, [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
                 const int slot = w.fl[slot0 + o];
                 // b[0] is structurally zero (lut.hpp:107-166): only orders 1..D are stored
@@ -698,6 +706,7 @@ class RayWorker {
         while (true) {
             // ---- gather: exact hit test of 32 candidates at a time
             while (hq_n < 32 && cursor < ce) {
+                SPHRAY_KS(kStatGather, 1);
                 const uint32_t c = cursor + lane;
                 bool hit = false;
                 double lam = 0.0, tchi = 0.0;
@@ -786,14 +795,15 @@ class RayWorker {
     }
 
     __device__ void finish(double* out) {
+        const double sr = warp_sum(Cr), sg = warp_sum(Cg), sb = warp_sum(Cb);
         if (lane == 0) {
             double r = P.bg[0], g = P.bg[1], b = P.bg[2];
             if (knots > 0) {
                 // pixel = C + (1 - a) * background, a = 1 - T (raycast.hpp:379, 486-488)
                 const double a = 1.0 - T;
-                r = Cr + (1.0 - a) * P.bg[0];
-                g = Cg + (1.0 - a) * P.bg[1];
-                b = Cb + (1.0 - a) * P.bg[2];
+                r = sr + (1.0 - a) * P.bg[0];
+                g = sg + (1.0 - a) * P.bg[1];
+                b = sb + (1.0 - a) * P.bg[2];
             }
             out[0] = r;
             out[1] = g;
@@ -880,10 +890,11 @@ __global__ void k_quantize_hits(const QuantParams Q, const sphray_particle* ps, 
         knot_count[i] = ovf ? -1 : 0;
         return;
     }
-    double X[2 * D];
+    double X[3 * D];
     for (int d = 1; d <= D; ++d) {
         X[d - 1] = dmul(dmul(powtau[d - 1], p.mass), p.value);
         X[D + d - 1] = dmul(dmul(Q.sigma, p.density), powh[i * D + d - 1]);
+        X[2 * D + d - 1] = recip_or_nan(X[D + d - 1]);
     }
     const int stride = Q.K + 1;
     quantize_emit<D, M>(Q, X, hp, ovf, [&](int o, int64_t t, const int64_t (&b)[D + 1]) {

@@ -1,0 +1,25 @@
+# A/B of library variants on one config (run under gpurun from repo root).
+# VARIANTS="name|lib|bench args;..."  (lib "-" = in-tree build)
+mkdir -p gpurun_out
+CFG=${CFG:-3}
+REPS=${REPS:-2}
+VARIANTS=${VARIANTS:-"new|-|"}
+for rep in $(seq 1 $REPS); do
+  IFS=';' read -ra VS <<< "$VARIANTS"
+  for v in "${VS[@]}"; do
+    IFS='|' read -r name lib args <<< "$v"
+    if [ "$lib" = "-" ]; then unset SPHRAY_B200_LIB; else export SPHRAY_B200_LIB=$PWD/$lib; fi
+    timeout 900 python bench.py --config $CFG --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 $args \
+      > gpurun_out/ab_${name}_${rep}.json 2> gpurun_out/ab_${name}_${rep}.err
+    python - "$name" "$rep" <<'PY' >> gpurun_out/ab_summary.txt
+import json,sys
+try:
+    d=json.loads(open(f"gpurun_out/ab_{sys.argv[1]}_{sys.argv[2]}.json").read().strip().splitlines()[-1])
+    print(sys.argv[1], sys.argv[2], round(d["value"],4), round(d["ms_per_step"],1), d.get("clocks",{}).get("sm_mhz"),
+          "retries", d.get("stats",{}).get("window_retries"))
+except Exception as e:
+    print(sys.argv[1], sys.argv[2], "FAILED", e)
+PY
+  done
+done
+cat gpurun_out/ab_summary.txt

@@ -55,6 +55,12 @@ def main():
             if other and ph in ("insert_hits",):
                 ph = "quantize(" + other[0][0] + ")"
             off2ph[int(m.group(1), 16)] = ph
+    if csvp == "-":  # static code size only
+        code = Counter(off2ph.values())
+        for ph, v in code.most_common():
+            print(f"{ph:28s} {v:6d}")
+        print(f"{'total':28s} {sum(code.values()):6d}")
+        return
     rows = list(csv.reader(open(csvp)))
     hdr = rows[1]
     I = {h: i for i, h in enumerate(hdr)}
@@ -70,8 +76,11 @@ def main():
         ex[ph] += int(r[I["Instructions Executed"]])
         st[ph] += int(r[I["Warp Stall Sampling (All Samples)"]])
     te, ts = sum(ex.values()), sum(st.values())
+    code = Counter(off2ph.values())
+    print(f"{'phase':28s} {'exec':>11s} {'stall':>13s} {'SASS instrs':>12s}")
     for ph, v in ex.most_common():
-        print(f"{ph:28s} exec {v / te * 100:5.1f}%   stall {st[ph] / ts * 100:5.1f}%")
+        print(f"{ph:28s} exec {v / te * 100:5.1f}%   stall {st[ph] / ts * 100:5.1f}%   {code[ph]:6d}")
+    print(f"{'total':28s} {'':11s} {'':13s}   {sum(code.values()):6d}")
 
 
 if __name__ == "__main__":
