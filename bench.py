@@ -306,7 +306,7 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (the render kernel)
     peaks, peak_src = measured_peaks()
     D = lut.D
-    per_particle = 32 + 16 + 4 + 16 * D  # x,y,z,h + bbox + front + X_d,Y_d
+    per_particle = 32 + 16 + 4 + 24 * D  # x,y,z,h + bbox + front + X_d, Y_d, 1/Y_d
     alg_bytes = (len(ps) * per_particle + st.candidates * (4 + 8) +
                  res * res * 3 * 8 / max(world, 1))
     achieved = alg_bytes / (render_ms * 1e-3) / 1e9

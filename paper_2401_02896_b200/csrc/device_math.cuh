@@ -69,6 +69,26 @@ __device__ __forceinline__ bool hit_ray(const RayD& r, double cx, double cy, dou
     return true;
 }
 
+// hit_ray split in two for the render kernel: the predicate returns d2 and
+// t_chi; lam_of(d2, h) is the RayHit::lam of the same hit, computed later
+// (per queued hit, not per tested candidate).
+__device__ __forceinline__ bool hit_test(const RayD& r, double cx, double cy, double cz,
+                                         double support, double near_plane, double far_plane,
+                                         double& d2_out, double& t_chi) {
+    const double ocx = dsub(cx, r.ox), ocy = dsub(cy, r.oy), ocz = dsub(cz, r.oz);
+    const double t = dadd(dadd(dmul(ocx, r.dx), dmul(ocy, r.dy)), dmul(ocz, r.dz));
+    const double d2 =
+        dsub(dadd(dadd(dmul(ocx, ocx), dmul(ocy, ocy)), dmul(ocz, ocz)), dmul(t, t));
+    if (!(d2 < dmul(support, support))) return false;
+    if (dadd(t, support) <= near_plane || dsub(t, support) >= far_plane) return false;
+    d2_out = d2;
+    t_chi = t;
+    return true;
+}
+__device__ __forceinline__ double lam_of(double d2, double h) {
+    return ddiv(dsqrt(d2 < 0.0 ? 0.0 : d2), h);
+}
+
 // Conservative pixel bbox of particle_ray_footprint (raycast.hpp:134-176).
 // Returns px0,px1,py0,py1 already clipped to the image (empty if px0 > px1).
 __device__ __forceinline__ int clamp_int(double v) {

@@ -18,6 +18,16 @@
 
 namespace sphray_b200 {
 
+namespace {
+// host twin of dev::recip_or_nan (device_math.cuh)
+double recip_or_nan(double b) {
+    const double y = 1.0 / b;
+    const double ay = std::fabs(y);
+    return (ay >= 0x1p-1000 && ay <= 0x1p1000) ? y : std::numeric_limits<double>::quiet_NaN();
+}
+
+}  // namespace
+
 #define CUDA_OK(x)                                                                 \
     do {                                                                           \
         cudaError_t e_ = (x);                                                      \
@@ -251,13 +261,6 @@ constexpr size_t kSmemLimit = 227 * 1024;
 }  // namespace
 
 namespace {
-// host twin of dev::recip_or_nan (device_math.cuh)
-double recip_or_nan(double b) {
-    const double y = 1.0 / b;
-    const double ay = std::fabs(y);
-    return (ay >= 0x1p-1000 && ay <= 0x1p1000) ? y : std::numeric_limits<double>::quiet_NaN();
-}
-
 // SPHRAY_TRACE=1: host-side phase timings of each frame on stderr
 struct Trace {
     bool on = std::getenv("SPHRAY_TRACE") != nullptr;
@@ -476,26 +479,72 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         }
         P.mode = SPHRAY_MODE_EXACT;
     }
-    // default window: 448 knot slots per ray (largest that keeps 11 warps/SM
-    // resident on B200 with D = 3; measured faster than 512 with no retries)
-    int cap = opts.window > 0 ? std::min(opts.window, 65535) : 448;
-    const size_t wb = warp_smem_bytes(D, cap, m);
-    if (wb > kSmemLimit) fail(SPHRAY_ERR_CONFIG, "knot window does not fit shared memory");
-    // CTA size: the warps-per-CTA that packs the most warps per SM (shared
-    // memory is the occupancy limiter; each warp carries its own window)
-    int warps = 1, bps = 0, best = 0;
-    for (int wpb : {4, 2, 8, 1}) {
-        if (wb * wpb > kSmemLimit) continue;
-        const int nb = max_blocks_per_sm(D, m, wpb, wb * wpb);
-        if (nb * wpb > best) {
-            best = nb * wpb;
-            warps = wpb;
-            bps = nb;
+    // Knot window and CTA shape.  Shared memory (the windows) and registers
+    // bound the resident warps; the default window is the largest of a few
+    // sizes that reaches the best warps/SM (windows below ~384 slots make
+    // config-3 rays overflow into the retry pass).
+    const size_t tfb_full = ntf * 6 * sizeof(double);
+    const size_t tfb = (tfb_full <= 4096 && !std::getenv("SPHRAY_TF_GLOBAL")) ? tfb_full : 0;
+    P.tf_smem = static_cast<int>(tfb);
+    auto best_shape = [&](int cap_, int& warps_, int& bps_) {
+        const size_t wb_ = warp_smem_bytes(D, cap_, m);
+        int best_ = 0;
+        warps_ = 1;
+        bps_ = 0;
+        for (int wpb : {4, 2, 8, 1, 3, 6}) {
+            if (wb_ * wpb + tfb > kSmemLimit) continue;
+            const int nb = max_blocks_per_sm(D, m, wpb, wb_ * wpb + tfb);
+            if (nb * wpb > best_) {
+                best_ = nb * wpb;
+                warps_ = wpb;
+                bps_ = nb;
+            }
+        }
+        return best_;
+    };
+    int cap = 0, warps = 1, bps = 0;
+    // validation dumps (hits / pieces) are written as rays run, so a ray must
+    // not be re-run: dump frames use the widest window from the start
+    const long long shape_key[4] = {D, m, static_cast<long long>(tfb), dumps ? -1 : opts.window};
+    if (std::equal(shape_key, shape_key + 4, shape_key_)) {
+        cap = shape_val_[0];
+        warps = shape_val_[1];
+        bps = shape_val_[2];
+    } else if (dumps) {
+        cap = 65535;
+        while (cap > 64 && warp_smem_bytes(D, cap, m) + tfb > kSmemLimit) cap = cap * 15 / 16;
+        best_shape(cap, warps, bps);
+    } else if (opts.window > 0) {
+        cap = std::min(opts.window, 65535);
+        if (warp_smem_bytes(D, cap, m) + tfb > kSmemLimit)
+            fail(SPHRAY_ERR_CONFIG, "knot window does not fit shared memory");
+        best_shape(cap, warps, bps);
+    } else {
+        int best = -1;
+        for (int c : {512, 480, 448, 432, 416, 400, 384}) {
+            int w_, b_;
+            const int r = best_shape(c, w_, b_);
+            if (r > best) {
+                best = r;
+                cap = c;
+                warps = w_;
+                bps = b_;
+            }
         }
     }
+    std::copy(shape_key, shape_key + 4, shape_key_);
+    shape_val_[0] = cap;
+    shape_val_[1] = warps;
+    shape_val_[2] = bps;
+    const size_t wb = warp_smem_bytes(D, cap, m);
+    if (const char* e = std::getenv("SPHRAY_BPS"))  // diagnostics: fewer CTAs per SM
+        bps = std::max(1, std::min(bps, std::atoi(e)));
     if (bps < 1) bps = 1;
     P.cap = cap;
     P.warp_bytes = static_cast<int>(wb);
+    if (trace.on)
+        trace.line += " cap=" + std::to_string(cap) + " warps/cta=" + std::to_string(warps) +
+                      " ctas/sm=" + std::to_string(bps);
     CUDA_OK(cudaMemsetAsync(d_work_.p, 0, 8, s));
     CUDA_OK(cudaMemsetAsync(d_retry_count_.p, 0, 8, s));
     CUDA_OK(cudaEventRecord(evr0_, s));
@@ -510,9 +559,12 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     CUDA_OK(cudaMemcpyAsync(&retry, d_retry_count_.p, 4, cudaMemcpyDeviceToHost, s));
     CUDA_OK(cudaStreamSynchronize(s));
     trace.mark("render");
+    if (retry > 0 && dumps)
+        fail(SPHRAY_ERR_CAPACITY, std::to_string(retry) + " rays exceed the widest knot window (" +
+                                      std::to_string(cap) + " knots)");
     if (retry > 0) {
         int cap2 = 65535;
-        while (cap2 > cap && warp_smem_bytes(D, cap2, m) > kSmemLimit) cap2 = cap2 * 15 / 16;
+        while (cap2 > cap && warp_smem_bytes(D, cap2, m) + tfb > kSmemLimit) cap2 = cap2 * 15 / 16;
         if (cap2 <= cap) fail(SPHRAY_ERR_CAPACITY, "knot window cannot grow");
         FrameParams P2 = P;
         P2.cap = cap2;
@@ -522,7 +574,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         P2.retry_list = d_retry2_.as<uint32_t>();
         P2.retry_count = d_retry_count_.as<unsigned int>() + 1;
         CUDA_OK(cudaMemsetAsync(d_work_.p, 0, 8, s));
-        int bps2 = max_blocks_per_sm(D, m, 1, P2.warp_bytes);
+        int bps2 = max_blocks_per_sm(D, m, 1, P2.warp_bytes + tfb);
         if (bps2 < 1) bps2 = 1;
         launch_render(P2, D, m, std::min<int>(retry, sm_count_ * bps2), 1, s);
         ++launches;
@@ -579,7 +631,8 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     trace.mark("tail");
     if (trace.on && (st[kStatFlushes] | st[kStatBatches])) {
         static const char* names[] = {"flushes", "scanned", "selected", "chunks", "radix_passes",
-                                      "batches", "samples", "balanced", "gather"};
+                                      "batches", "samples", "balanced", "gather", "resid<128",
+                                      "resid<192", "resid<256", "resid<320", "resid<384", "resid>=384"};
         for (int k = kStatFirstK; k < kStatCount; ++k)
             trace.line += std::string(" ") + names[k - kStatFirstK] + "=" + std::to_string(st[k]);
     }

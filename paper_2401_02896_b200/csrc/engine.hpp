@@ -92,6 +92,8 @@ class Engine {
         d_dump_pa_, d_stats_all_;
     HostPinned h_stage_;
     std::vector<double> h_powh_;
+    long long shape_key_[4] = {-1, -1, -1, -1};  // render CTA shape cache (D, m, tf bytes, window)
+    int shape_val_[3] = {0, 0, 0};
     std::vector<double> h_tf_;
 };
 

@@ -29,8 +29,8 @@ SPHRAY_HD inline size_t warp_bytes_for(int D, int cap) {
     size_t b = 0;
     b += align16(sizeof(uint64_t) * (D + 1) * cap);  // pool: t + orders 1..D
     b += align16(sizeof(uint64_t) * 32);              // na0
-    b += align16(sizeof(double) * kHitQueue * 2);     // hit queue
-    b += align16(sizeof(int32_t) * kHitQueue * 2);
+    b += align16(sizeof(double) * kHitQueue * 2);     // hit queue: d2, t_chi
+    b += align16(sizeof(int32_t) * kHitQueue);        // hit queue: particle
     b += align16(sizeof(uint16_t) * cap * 3);         // ps, fl, fs
     b += align16(sizeof(uint16_t) * 32);              // pcs
     b += align16(sizeof(uint32_t) * 256);             // radix bins
@@ -76,6 +76,7 @@ struct FrameParams {
     // knot window
     int cap;         // knot slots per warp
     int warp_bytes;  // dynamic smem per warp
+    int tf_smem;     // bytes of the per-CTA shared copy of tf after the windows (0: read global)
     // work distribution
     unsigned long long* work_counter;
     uint64_t total_work;
@@ -117,7 +118,8 @@ enum StatIndex {
     kStatSamples = 14,   // composited samples (lane path + balanced path)
     kStatBalanced = 15,  // chunks sent to the sample-parallel path
     kStatGather = 16,    // 32-candidate gather iterations
-    kStatCount = 17
+    kStatPeak0 = 17,     // rays by largest post-flush residual: <128, <192, <256, <320, <384, >=384
+    kStatCount = 23
 };
 constexpr int kStatFirstK = kStatFlushes;
 

@@ -76,32 +76,46 @@ __device__ __forceinline__ int64_t knot_floor(float front, double tau) {
 // (<= 1 ulp from the reference's division; inside the RGB tolerance).
 constexpr int kTfStride = 6;
 
-__device__ __forceinline__ void tf_sample(const double* tf, int n, double v, double& r, double& g,
+// TF readers: the per-CTA shared copy (ld.shared) or global memory.
+struct TfShared {
+    uint32_t base;
+    __device__ __forceinline__ double operator()(int k) const {
+        double v;
+        asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(base + 8u * static_cast<uint32_t>(k)));
+        return v;
+    }
+};
+struct TfGlobal {
+    const double* p;
+    __device__ __forceinline__ double operator()(int k) const { return __ldg(p + k); }
+};
+
+template <class Ld>
+__device__ __forceinline__ void tf_sample(const Ld& ld, int n, double v, double& r, double& g,
                                           double& b, double& ab) {
-    if (v <= tf[0]) {
-        r = tf[1];
-        g = tf[2];
-        b = tf[3];
-        ab = tf[4];
+    if (v <= ld(0)) {
+        r = ld(1);
+        g = ld(2);
+        b = ld(3);
+        ab = ld(4);
         return;
     }
-    const double* last = tf + kTfStride * (n - 1);
-    if (v >= last[0]) {
-        r = last[1];
-        g = last[2];
-        b = last[3];
-        ab = last[4];
+    const int last = kTfStride * (n - 1);
+    if (v >= ld(last)) {
+        r = ld(last + 1);
+        g = ld(last + 2);
+        b = ld(last + 3);
+        ab = ld(last + 4);
         return;
     }
-    int i = 1;
-    while (tf[kTfStride * i] < v) ++i;
-    const double* A = tf + kTfStride * (i - 1);
-    const double* B = A + kTfStride;
-    const double w = (v - A[0]) * A[5];
-    r = fma(w, B[1] - A[1], A[1]);
-    g = fma(w, B[2] - A[2], A[2]);
-    b = fma(w, B[3] - A[3], A[3]);
-    ab = fma(w, B[4] - A[4], A[4]);
+    int i = kTfStride;
+    while (ld(i) < v) i += kTfStride;
+    const int A = i - kTfStride;
+    const double w = (v - ld(A)) * ld(A + 5);
+    r = fma(w, ld(i + 1) - ld(A + 1), ld(A + 1));
+    g = fma(w, ld(i + 2) - ld(A + 2), ld(A + 2));
+    b = fma(w, ld(i + 3) - ld(A + 3), ld(A + 3));
+    ab = fma(w, ld(i + 4) - ld(A + 4), ld(A + 4));
 }
 
 // n = max(2, ceil((hi - lo) / step)) exactly as the reference counts samples
@@ -176,9 +190,8 @@ __device__ __forceinline__ void bitonic_sort(uint64_t (&k)[R], int lane) {
 struct WarpMem {
     uint64_t* pool;  // (D+1) x cap, SoA (see the file comment)
     uint64_t* na0;   // 32: order-0 coefficients of the pieces of a chunk
-    double* hq_lam;  // hit queue (candidate order)
+    double* hq_d2;  // hit queue (candidate order): squared distance of closest approach
     double* hq_t;
-    int32_t* hq_c;
     int32_t* hq_p;
     uint16_t* ps;   // pending slots, unsorted
     uint16_t* fl;   // free slot stack
@@ -195,12 +208,11 @@ __device__ inline WarpMem carve(char* base, int D, int cap) {
     p += align16(sizeof(uint64_t) * (D + 1) * cap);
     w.na0 = reinterpret_cast<uint64_t*>(p);
     p += align16(sizeof(uint64_t) * 32);
-    w.hq_lam = reinterpret_cast<double*>(p);
-    w.hq_t = w.hq_lam + kHitQueue;
+    w.hq_d2 = reinterpret_cast<double*>(p);
+    w.hq_t = w.hq_d2 + kHitQueue;
     p += align16(sizeof(double) * kHitQueue * 2);
-    w.hq_c = reinterpret_cast<int32_t*>(p);
-    w.hq_p = w.hq_c + kHitQueue;
-    p += align16(sizeof(int32_t) * kHitQueue * 2);
+    w.hq_p = reinterpret_cast<int32_t*>(p);
+    p += align16(sizeof(int32_t) * kHitQueue);
     w.ps = reinterpret_cast<uint16_t*>(p);
     w.fl = w.ps + cap;
     w.fs = w.fl + cap;
@@ -211,14 +223,16 @@ __device__ inline WarpMem carve(char* base, int D, int cap) {
     return w;
 }
 
-// One warp renders one ray at a time.
-template <int D, int M>
+// One warp renders one ray at a time.  TS: the transfer function is read
+// from the CTA's shared copy (else from global memory).
+template <int D, int M, bool TS>
 class RayWorker {
    public:
     static constexpr int KN = 2 * M + 1;  // knots per hit, at most
     const FrameParams& P;
     WarpMem w;
     int lane;
+    uint32_t tf_sa;  // shared address of the CTA's TF copy (TS)
     uint64_t ray_id = 0;
     // warp-uniform ray state
     int np = 0, nfree = 0;
@@ -233,8 +247,10 @@ class RayWorker {
     bool term = false;
     unsigned long long knots = 0, pieces = 0, hits = 0;
     int max_pending = 0;
+    int max_resid = 0;  // SPHRAY_KSTATS: largest pending set left by a flush
 
-    __device__ RayWorker(const FrameParams& p, WarpMem wm, int l) : P(p), w(wm), lane(l) {}
+    __device__ RayWorker(const FrameParams& p, WarpMem wm, int l, uint32_t t)
+        : P(p), w(wm), lane(l), tf_sa(t) {}
 
     __device__ __forceinline__ int64_t pool_t(int slot) const {
         return static_cast<int64_t>(w.pool[slot]);
@@ -259,6 +275,7 @@ class RayWorker {
         term = false;
         knots = pieces = hits = 0;
         max_pending = 0;
+        max_resid = 0;
         __syncwarp();
     }
 
@@ -285,7 +302,10 @@ class RayWorker {
 #pragma unroll
         for (int d = D - 1; d >= 0; --d) acc = fma(acc, x, c[d]);
         double ab;
-        tf_sample(P.tf, P.ntf, acc, r, g, b, ab);
+        if constexpr (TS)
+            tf_sample(TfShared{tf_sa}, P.ntf, acc, r, g, b, ab);
+        else
+            tf_sample(TfGlobal{P.tf}, P.ntf, acc, r, g, b, ab);
         alpha = alpha_of(ab * dt);
     }
 
@@ -468,7 +488,8 @@ class RayWorker {
 
     // Sort fs[0, nsel) by knot position: warp LSD radix sort on (t - tmin),
     // 8 bits per pass (flush sets usually span < 2^16 tau: two passes).  The
-    // scatter is stable: ranks within a round of 32 come from match.any.
+    // scatter is stable: ranks within a round of 32 come from match.any (a
+    // per-bit ballot version measured 2% slower).
     __device__ void sort_flush_radix(int nsel, int64_t tmin, int bits) {
         uint16_t* src = w.fs;
         uint16_t* dst = w.ps + np;  // free scratch: np + nsel <= cap
@@ -503,8 +524,8 @@ class RayWorker {
                 const int sl = valid ? src[i] : 0;
                 const uint32_t dg = valid ? static_cast<uint32_t>(
                     ((static_cast<uint64_t>(pool_t(sl)) - static_cast<uint64_t>(tmin)) >> shift) & 255u)
-                                          : 256u + lane;
-                const unsigned peers = __match_any_sync(kFull, dg);
+                                          : 0u;
+                const unsigned peers = __match_any_sync(kFull, valid ? dg : 256u + lane);
                 const unsigned below = peers & lanemask_lt();
                 const uint32_t base = valid ? w.hist[dg] : 0u;
                 __syncwarp();
@@ -575,6 +596,7 @@ class RayWorker {
         SPHRAY_KS(kStatSelected, nsel);
         SPHRAY_KS(kStatChunks, (nsel + 31) / 32);
         np = nkeep;
+        if (SPHRAY_KSTATS && np > max_resid) max_resid = np;
         if (nsel == 0) return;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -651,9 +673,9 @@ class RayWorker {
         double lam = 0.0, tchi = 0.0, h = 0.0;
         if (act) {
             pi = w.hq_p[lane];
-            lam = w.hq_lam[lane];
             tchi = w.hq_t[lane];
             h = P.pxyzh[pi].w;
+            lam = lam_of(w.hq_d2[lane], h);  // RayHit::lam, raycast.hpp:118
         }
         bool ovf = false;
         HitPositions<M> hp;
@@ -709,23 +731,22 @@ class RayWorker {
                 SPHRAY_KS(kStatGather, 1);
                 const uint32_t c = cursor + lane;
                 bool hit = false;
-                double lam = 0.0, tchi = 0.0;
+                double d2 = 0.0, tchi = 0.0;
                 uint32_t pi = 0;
                 if (c < ce) {
                     pi = P.cand[c];
                     const int4 bb = P.bbox[pi];
                     if (px >= bb.x && px <= bb.y && py >= bb.z && py <= bb.w) {
                         const double4 p = P.pxyzh[pi];
-                        hit = hit_ray(ray, p.x, p.y, p.z, dmul(P.Q.q, p.w), p.w, near_plane,
-                                      far_plane, lam, tchi);
+                        hit = hit_test(ray, p.x, p.y, p.z, dmul(P.Q.q, p.w), near_plane, far_plane,
+                                       d2, tchi);
                     }
                 }
                 const unsigned m = __ballot_sync(kFull, hit);
                 if (hit) {
                     const int at = hq_n + __popc(m & lanemask_lt());
-                    w.hq_c[at] = static_cast<int32_t>(c);
                     w.hq_p[at] = static_cast<int32_t>(pi);
-                    w.hq_lam[at] = lam;
+                    w.hq_d2[at] = d2;
                     w.hq_t[at] = tchi;
                 }
                 if (P.dump_hit_ray && m) {
@@ -738,7 +759,7 @@ class RayWorker {
                         if (at < P.dump_cap_hits) {
                             P.dump_hit_ray[at] = ray_id;
                             P.dump_hit_pidx[at] = P.orig[pi];
-                            P.dump_hit_lam[at] = lam;
+                            P.dump_hit_lam[at] = lam_of(d2, P.pxyzh[pi].w);
                             P.dump_hit_tchi[at] = tchi;
                         }
                     }
@@ -755,8 +776,10 @@ class RayWorker {
             const bool final_ = hq_n == 0 && cursor >= ce;
             int64_t F = INT64_MAX;
             if (!final_) {
-                const uint32_t next = hq_n > 0 ? static_cast<uint32_t>(w.hq_c[0]) : cursor;
-                F = knot_floor(P.front[P.cand[next]], P.Q.tau);
+                // candidates and queued hits are in front order: the first
+                // unprocessed one bounds every knot still to come
+                const uint32_t pn = hq_n > 0 ? static_cast<uint32_t>(w.hq_p[0]) : P.cand[cursor];
+                F = knot_floor(P.front[pn], P.Q.tau);
             }
             if (final_ || nfree < 32 * KN || np >= (P.cap >> 1)) flush(F, final_);
             if (final_) break;
@@ -771,19 +794,17 @@ class RayWorker {
                 const int rest = hq_n - nq;
                 for (int c0 = 0; c0 < rest; c0 += 32) {
                     const int i = c0 + lane;
-                    int32_t qc = 0, qp = 0;
+                    int32_t qp = 0;
                     double ql = 0.0, qt = 0.0;
                     if (i < rest) {
-                        qc = w.hq_c[nq + i];
                         qp = w.hq_p[nq + i];
-                        ql = w.hq_lam[nq + i];
+                        ql = w.hq_d2[nq + i];
                         qt = w.hq_t[nq + i];
                     }
                     __syncwarp();
                     if (i < rest) {
-                        w.hq_c[i] = qc;
                         w.hq_p[i] = qp;
-                        w.hq_lam[i] = ql;
+                        w.hq_d2[i] = ql;
                         w.hq_t[i] = qt;
                     }
                     __syncwarp();
@@ -827,18 +848,30 @@ class RayWorker {
             }
             if (hits) atomicAdd(&P.stats[kStatHits], hits);
             atomicMax(&P.stats[kStatMaxPending], static_cast<unsigned long long>(max_pending));
+            if (SPHRAY_KSTATS) {
+                const int b = max_resid < 128 ? 0 : max_resid < 192 ? 1 : max_resid < 256 ? 2
+                            : max_resid < 320 ? 3 : max_resid < 384 ? 4 : 5;
+                atomicAdd(&P.stats[kStatPeak0 + b], 1ull);
+            }
         }
         __syncwarp();
     }
 };
 
-template <int D, int M>
+template <int D, int M, bool TS>
 __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const FrameParams P) {
     extern __shared__ __align__(16) char smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const WarpMem wm = carve(smem + static_cast<size_t>(warp) * P.warp_bytes, D, P.cap);
-    RayWorker<D, M> rw(P, wm, lane);
+    uint32_t tf_sa = 0;
+    if constexpr (TS) {
+        double* st = reinterpret_cast<double*>(smem + static_cast<size_t>(blockDim.x >> 5) * P.warp_bytes);
+        for (int i = threadIdx.x; i < P.ntf * kTfStride; i += blockDim.x) st[i] = P.tf[i];
+        __syncthreads();
+        tf_sa = static_cast<uint32_t>(__cvta_generic_to_shared(st));
+    }
+    RayWorker<D, M, TS> rw(P, wm, lane, tf_sa);
     while (true) {
         unsigned long long item = 0;
         if (lane == 0) item = atomicAdd(P.work_counter, 1ull);
@@ -918,21 +951,21 @@ __global__ void k_quantize_hits(const QuantParams Q, const sphray_particle* ps, 
 template <int D, int M>
 int render_occupancy_t(int warps, size_t smem) {
     int nb = 0;
-    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(rk::k_render_rays<D, M>,
+    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(rk::k_render_rays<D, M, true>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
-    SPHRAY_RK_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, rk::k_render_rays<D, M>,
+    SPHRAY_RK_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, rk::k_render_rays<D, M, true>,
                                                                     warps * 32, smem));
     return nb;
 }
 
 template <int D, int M>
 void launch_render_t(const FrameParams& P, int blocks, int warps, cudaStream_t s) {
-    const size_t smem = static_cast<size_t>(P.warp_bytes) * warps;
-    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(rk::k_render_rays<D, M>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const size_t smem = static_cast<size_t>(P.warp_bytes) * warps + P.tf_smem;
+    auto kern = P.tf_smem ? rk::k_render_rays<D, M, true> : rk::k_render_rays<D, M, false>;
+    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
-    rk::k_render_rays<D, M><<<blocks, warps * 32, smem, s>>>(P);
+    kern<<<blocks, warps * 32, smem, s>>>(P);
     SPHRAY_RK_CUDA_OK(cudaGetLastError());
 }
 

@@ -1,5 +1,5 @@
 # A/B of library variants on one config (run under gpurun from repo root).
-# VARIANTS="name|lib|bench args;..."  (lib "-" = in-tree build)
+# VARIANTS="name|lib|bench args|ENV=v ...;..."  (lib "-" = in-tree build)
 mkdir -p gpurun_out
 CFG=${CFG:-3}
 REPS=${REPS:-2}
@@ -7,9 +7,9 @@ VARIANTS=${VARIANTS:-"new|-|"}
 for rep in $(seq 1 $REPS); do
   IFS=';' read -ra VS <<< "$VARIANTS"
   for v in "${VS[@]}"; do
-    IFS='|' read -r name lib args <<< "$v"
+    IFS='|' read -r name lib args envs <<< "$v"
     if [ "$lib" = "-" ]; then unset SPHRAY_B200_LIB; else export SPHRAY_B200_LIB=$PWD/$lib; fi
-    timeout 900 python bench.py --config $CFG --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 $args \
+    timeout 900 env $envs python bench.py --config $CFG --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 $args \
       > gpurun_out/ab_${name}_${rep}.json 2> gpurun_out/ab_${name}_${rep}.err
     python - "$name" "$rep" <<'PY' >> gpurun_out/ab_summary.txt
 import json,sys

@@ -291,3 +291,57 @@ def test_sharded_tiles_match_single_gpu(name, nranks):
     assert (rgb == img.pixels).all()
     for k, v in sums.items():
         assert v == getattr(st, k), k
+
+
+def _ulps(x, j):
+    """x moved by j ulps."""
+    x = np.asarray(x, np.float64)
+    return np.nextafter(x, np.where(j >= 0, np.inf, -np.inf)) if abs(j) == 1 else \
+        _ulps(np.nextafter(x, np.where(j >= 0, np.inf, -np.inf)), j - np.sign(j))
+
+
+@pytest.mark.parametrize("lutname", [(4, 3, 1024), (5, 4, 64)])
+def test_quantize_near_ties_live_reference(ctx, lutname):
+    """The quantize divisions run as reciprocal multiplies with an exactness
+    guard (device_math.cuh rint_div / lut_index).  Hits built to land within a
+    few ulps of the rounding boundaries -- t_chi/tau at half-integers,
+    h*u_k/tau at half-integers, lam/dl at LUT entry edges and lam = 0 -- must
+    still quantize bit-identically to the reference (oracle/_ref live)."""
+    path = H.lut_path(*lutname)
+    lut, rl = S.load_lut(path), ref.Lut(path)
+    rng = np.random.default_rng(5)
+    tau, sigma = 1.0 / 1000, 2.0 ** -40  # |coefficients| up to ~2^53: both paths
+    dl = lut.q / lut.N
+    rec = lut.records()
+    m = (lut.K + 1) // 2
+    n = 3000
+    ps = np.zeros((n, 7))
+    ps[:, 3] = rng.uniform(0.5, 2.0, n)       # mass
+    ps[:, 4] = rng.uniform(0.5, 2.0, n)       # density
+    ps[:, 5] = rng.uniform(0.01, 0.1, n)      # h
+    ps[:, 6] = rng.uniform(-1.0, 1.0, n)      # value
+    e = rng.integers(0, lut.N, n)
+    lam = e * dl
+    k = rng.integers(-4000, 4000, n)
+    tchi = (k + 0.5) * tau
+    j = rng.integers(-3, 4, n)
+    kind = np.arange(n) % 4
+    for i in range(n):
+        if kind[i] == 0 and j[i] != 0:      # t_chi / tau near a half-integer
+            tchi[i] = _ulps(tchi[i], int(j[i]))
+        elif kind[i] == 1:                  # lam / dl near an entry edge (or 0)
+            lam[i] = 0.0 if j[i] == 0 or e[i] == 0 else _ulps(lam[i], int(j[i]))
+        elif kind[i] == 2:                  # h * u_1 / tau near a half-integer
+            u1 = rec[min(e[i], lut.N - 1), 2]
+            h = (rng.integers(20, 200) + 0.5) * tau / u1
+            ps[i, 5] = h if j[i] == 0 else float(_ulps(h, int(j[i])))
+            lam[i] = (e[i] + 0.5) * dl
+    lam = np.minimum(lam, lut.q * (1 - 1e-12))
+    kt, kb, kc = ctx.quantize_hits(ps, tchi, lam, lut, S.QuantaConfig(tau, sigma, 64))
+    rqc = ref.RpQuanta(tau, sigma, 64)
+    D1 = lut.D + 1
+    for i in range(n):
+        rt, rb = ref.quantize(ps[i], 0, float(tchi[i]), float(lam[i]), rl, rqc)
+        assert kc[i] == len(rt), i
+        np.testing.assert_array_equal(kt[i, : kc[i]], rt, err_msg=str(i))
+        np.testing.assert_array_equal(kb[i, : kc[i]], rb[:, :D1], err_msg=str(i))
