@@ -559,6 +559,8 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     CUDA_OK(cudaMemcpyAsync(&retry, d_retry_count_.p, 4, cudaMemcpyDeviceToHost, s));
     CUDA_OK(cudaStreamSynchronize(s));
     trace.mark("render");
+    // diagnostics (ncu captures of the main launch only): skip the retry pass
+    if (std::getenv("SPHRAY_PROFILE_NO_RETRY")) retry = 0;
     if (retry > 0 && dumps)
         fail(SPHRAY_ERR_CAPACITY, std::to_string(retry) + " rays exceed the widest knot window (" +
                                       std::to_string(cap) + " knots)");

@@ -27,12 +27,12 @@ SPHRAY_HD inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 SPHRAY_HD inline size_t warp_bytes_for(int D, int cap) {
     size_t b = 0;
-    b += align16(sizeof(uint64_t) * (D + 1) * cap);  // pool: t + orders 1..D
-    b += align16(sizeof(uint64_t) * 32);              // na0
+    b += align16(sizeof(uint64_t) * D * cap);        // pool: jumps of orders 1..D
+    b += align16(sizeof(uint32_t) * cap);            // pt: position offsets
+    b += align16(sizeof(uint64_t) * (D + 2));         // open piece
     b += align16(sizeof(double) * kHitQueue * 2);     // hit queue: d2, t_chi
     b += align16(sizeof(int32_t) * kHitQueue);        // hit queue: particle
-    b += align16(sizeof(uint16_t) * cap * 3);         // ps, fl, fs
-    b += align16(sizeof(uint16_t) * 32);              // pcs
+    b += align16(sizeof(uint16_t) * cap * 2);         // ps, fl (+ flush set)
     b += align16(sizeof(uint32_t) * 256);             // radix bins
     return b;
 }

@@ -4,13 +4,17 @@
 // compile in parallel.  See render.cu for the reference mapping.
 //
 // Per-ray knot window (shared memory, one per warp):
-//   pool   (D+1) x cap u64: row 0 = knot position t, rows 1..D = the knot's
-//          jumps (order 0 is structurally zero) -- or, once the knot has
-//          become a FieldPiece, its merged coefficients of orders 1..D
+//   pt     cap u32: knot position as an offset from the ray's base tb (the
+//          first flush bound: every knot of the ray is >= it)
+//   pool   D x cap u64: the knot's jumps of orders 1..D (order 0 is
+//          structurally zero)
 //   ps     pending knots (slot ids), UNSORTED: inserting a batch is an append
-//   fs     the flush set: pending knots with t < F, selected by a ballot scan
-//          and sorted (packed-key warp bitonic) only when they are final
-//   fl     free-slot stack;  pcs/na0  the pieces of one 32-knot chunk
+//   fl     free-slot stack [0, nfree); directly above it, during a flush, the
+//          flush set fs = fl + nfree: pending knots with t < F, selected by a
+//          ballot scan and sorted (warp LSD radix) only when they are final;
+//          once merged they are free slots already (nfree += nsel)
+//   open   the last piece (t, a_0..a_D), whose end is the first knot of the
+//          next flush set
 #pragma once
 
 #include <cuda_runtime.h>
@@ -124,7 +128,7 @@ __device__ __forceinline__ void tf_sample(const Ld& ld, int n, double v, double&
 __device__ __forceinline__ int sample_count(double len, double step, double inv_step) {
     const double q = len * inv_step;
     double c = ceil(q);
-    if (fabs(q - rint(q)) <= 1e-12 * q + 1e-300) c = ceil(ddiv(len, step));
+    if (fabs(q - rint(q)) <= 1e-12 * q + 1e-300) c = ceil(div_exact(len, step));
     return c > 2.0 ? static_cast<int>(c) : 2;
 }
 
@@ -136,9 +140,6 @@ __device__ __forceinline__ double alpha_of(double x) {
     return 1.0 - static_cast<double>(__expf(-static_cast<float>(x)));
 }
 
-constexpr int kLaneSamples = 8;  // pieces up to this many samples are sampled lane-locally
-__constant__ double c_inv_small[kLaneSamples + 1] = {0.0, 1.0, 1.0 / 2, 1.0 / 3, 1.0 / 4,
-                                                     1.0 / 5, 1.0 / 6, 1.0 / 7, 1.0 / 8};
 
 // Warp bitonic sort of 32*R u64 keys held R per lane (blocked layout:
 // element e = lane*R + r), ascending.  The (size, stride) stage loop is a
@@ -188,15 +189,14 @@ __device__ __forceinline__ void bitonic_sort(uint64_t (&k)[R], int lane) {
 }
 
 struct WarpMem {
-    uint64_t* pool;  // (D+1) x cap, SoA (see the file comment)
-    uint64_t* na0;   // 32: order-0 coefficients of the pieces of a chunk
+    uint32_t* pt;    // cap: position offsets (see the file comment)
+    uint64_t* pool;  // D x cap: jumps of orders 1..D
+    uint64_t* open;  // D+2: the open piece (t, a_0..a_D)
     double* hq_d2;  // hit queue (candidate order): squared distance of closest approach
     double* hq_t;
     int32_t* hq_p;
     uint16_t* ps;   // pending slots, unsorted
-    uint16_t* fl;   // free slot stack
-    uint16_t* fs;   // flush set slots (sorted by t)
-    uint16_t* pcs;   // 32: slots of the pieces of a chunk
+    uint16_t* fl;   // free slot stack (+ the flush set above it)
     uint32_t* hist;  // 256: radix-sort bins
 };
 
@@ -205,9 +205,11 @@ __device__ inline WarpMem carve(char* base, int D, int cap) {
     WarpMem w;
     char* p = base;
     w.pool = reinterpret_cast<uint64_t*>(p);
-    p += align16(sizeof(uint64_t) * (D + 1) * cap);
-    w.na0 = reinterpret_cast<uint64_t*>(p);
-    p += align16(sizeof(uint64_t) * 32);
+    p += align16(sizeof(uint64_t) * D * cap);
+    w.pt = reinterpret_cast<uint32_t*>(p);
+    p += align16(sizeof(uint32_t) * cap);
+    w.open = reinterpret_cast<uint64_t*>(p);
+    p += align16(sizeof(uint64_t) * (D + 2));
     w.hq_d2 = reinterpret_cast<double*>(p);
     w.hq_t = w.hq_d2 + kHitQueue;
     p += align16(sizeof(double) * kHitQueue * 2);
@@ -215,10 +217,7 @@ __device__ inline WarpMem carve(char* base, int D, int cap) {
     p += align16(sizeof(int32_t) * kHitQueue);
     w.ps = reinterpret_cast<uint16_t*>(p);
     w.fl = w.ps + cap;
-    w.fs = w.fl + cap;
-    p += align16(sizeof(uint16_t) * cap * 3);
-    w.pcs = reinterpret_cast<uint16_t*>(p);
-    p += align16(sizeof(uint16_t) * 32);
+    p += align16(sizeof(uint16_t) * cap * 2);
     w.hist = reinterpret_cast<uint32_t*>(p);
     return w;
 }
@@ -236,12 +235,13 @@ class RayWorker {
     uint64_t ray_id = 0;
     // warp-uniform ray state
     int np = 0, nfree = 0;
+    uint16_t* fs = nullptr;  // flush set of the current flush (w.fl + nfree)
+    int64_t tb = 0;          // position base of pt[]
+    bool has_base = false;
     uint64_t G[D + 1];  // running sum of jumps shifted to tref (mod 2^64)
     int64_t tref = 0;
     bool has_ref = false;
-    int open_slot = 0;     // last piece: its successor is not known yet
-    uint64_t open_a0 = 0;  // its order-0 coefficient (the slot holds orders 1..D)
-    bool has_open = false;
+    bool has_open = false;  // w.open holds the last piece
     double T = 1.0;
     double Cr = 0.0, Cg = 0.0, Cb = 0.0;  // per-lane partial colour sums (reduced in finish)
     bool term = false;
@@ -253,10 +253,10 @@ class RayWorker {
         : P(p), w(wm), lane(l), tf_sa(t) {}
 
     __device__ __forceinline__ int64_t pool_t(int slot) const {
-        return static_cast<int64_t>(w.pool[slot]);
+        return tb + static_cast<int64_t>(w.pt[slot]);
     }
     __device__ __forceinline__ uint64_t& pool_c(int d, int slot) const {
-        return w.pool[d * P.cap + slot];
+        return w.pool[(d - 1) * P.cap + slot];
     }
 
     __device__ void reset() {
@@ -267,22 +267,15 @@ class RayWorker {
         for (int d = 0; d <= D; ++d) G[d] = 0;
         tref = 0;
         has_ref = false;
-        open_slot = 0;
-        open_a0 = 0;
         has_open = false;
+        tb = 0;
+        has_base = false;
         T = 1.0;
         Cr = Cg = Cb = 0.0;
         term = false;
         knots = pieces = hits = 0;
         max_pending = 0;
         max_resid = 0;
-        __syncwarp();
-    }
-
-    __device__ void free_slots(bool give, int slot) {
-        const unsigned m = __ballot_sync(kFull, give);
-        if (give) w.fl[nfree + __popc(m & lanemask_lt())] = static_cast<uint16_t>(slot);
-        nfree += __popc(m);
         __syncwarp();
     }
 
@@ -327,140 +320,164 @@ class RayWorker {
         }
     }
 
-    // Composite the pieces completed in this chunk: lane j (j < cp) takes the
-    // piece that starts at the previous piece (the carried open piece for
-    // j == 0) and ends at chunk piece j.  Each lane samples its own piece
-    // sequentially; one warp combine (prefix product of transmittances,
-    // weighted colour sum) then folds the chunk into the ray.  Pieces with
-    // many samples (long gaps) go through a sample-parallel path instead.
-    __device__ void composite_chunk(int cp) {
-        const bool have = lane < cp && (lane > 0 || has_open);
-        int64_t ts = 0, te = 0;
-        int slot = 0;
-        uint64_t a0 = 0;
-        if (lane < cp) {
-            te = pool_t(w.pcs[lane]);
-            slot = lane == 0 ? open_slot : w.pcs[lane - 1];
-            a0 = lane == 0 ? open_a0 : w.na0[lane - 1];
-            ts = pool_t(slot);
+    // Per-piece setup of composite() (raycast.hpp:364-372): [lo, hi] =
+    // [t_s tau, t_e tau] cut to [near, far], n = max(2, ceil((hi-lo)/step))
+    // samples of width dt = (hi-lo)/n, the piece polynomial in double scaled
+    // by sigma, and the piece-local abscissa x0 + (s + 1/2) dx of sample s.
+    // Returns 0 when nothing is sampled (empty interval, or a zero piece
+    // under a transfer function that is clear at 0: alpha = 1 - exp(-0) = 0).
+    __device__ __forceinline__ int piece_setup(int64_t ts, int64_t te, const uint64_t (&a)[D + 1],
+                                               double (&c)[D + 1], double& x0, double& dx,
+                                               double& dt) const {
+        const double a_lo = dmul(static_cast<double>(ts), P.Q.tau);
+        const double a_hi = dmul(static_cast<double>(te), P.Q.tau);
+        const double lo = (a_lo < P.cam.near_plane) ? P.cam.near_plane : a_lo;
+        const double hi = (P.cam.far_plane < a_hi) ? P.cam.far_plane : a_hi;
+        if (!(hi > lo)) return 0;
+        const double len = dsub(hi, lo);
+        const int n = sample_count(len, P.step, P.inv_step);
+        dt = n == 2 ? len * 0.5 : div_exact(len, static_cast<double>(n));
+        bool zero = true;
+#pragma unroll
+        for (int d = 0; d <= D; ++d) {
+            zero &= a[d] == 0;
+            c[d] = static_cast<double>(static_cast<int64_t>(a[d])) * P.Q.sigma;
         }
-        const int last_slot = __shfl_sync(kFull, lane < cp ? static_cast<int>(w.pcs[lane]) : 0, cp - 1);
-        const uint64_t last_a0 = __shfl_sync(kFull, lane < cp ? w.na0[lane] : 0ull, cp - 1);
-
-        if (!term) {
-            int n = 0;
-            double lo = 0.0, dt = 0.0, x0 = 0.0, dx = 0.0;
-            double c[D + 1];
-#pragma unroll
-            for (int d = 0; d <= D; ++d) c[d] = 0.0;
-            if (have) {
-                // [lo, hi] = [t_i tau, t_{i+1} tau] cut to [near, far]   (raycast.hpp:364-368)
-                const double a_lo = dmul(static_cast<double>(ts), P.Q.tau);
-                const double a_hi = dmul(static_cast<double>(te), P.Q.tau);
-                lo = (a_lo < P.cam.near_plane) ? P.cam.near_plane : a_lo;
-                const double hi = (P.cam.far_plane < a_hi) ? P.cam.far_plane : a_hi;
-                if (hi > lo) {
-                    const double len = dsub(hi, lo);
-                    n = sample_count(len, P.step, P.inv_step);
-                    dt = n <= kLaneSamples ? len * c_inv_small[n] : len / static_cast<double>(n);
-                    bool zero = a0 == 0;
-                    c[0] = static_cast<double>(static_cast<int64_t>(a0)) * P.Q.sigma;
-#pragma unroll
-                    for (int d = 1; d <= D; ++d) {
-                        const int64_t a = static_cast<int64_t>(pool_c(d, slot));
-                        zero &= a == 0;
-                        c[d] = static_cast<double>(a) * P.Q.sigma;
-                    }
-                    x0 = fma(lo, P.inv_tau, -static_cast<double>(ts));
-                    dx = dt * P.inv_tau;
-                    // alpha = 1 - exp(-0) = 0 exactly: no colour, T unchanged
-                    if (zero && P.tf0_clear) n = 0;
-                }
-            }
-            const int maxn = __reduce_max_sync(kFull, n);
-            if (SPHRAY_KSTATS) {
-                const unsigned ns = __reduce_add_sync(kFull, static_cast<unsigned>(n));
-                SPHRAY_KS(kStatSamples, ns);
-            }
-            if (maxn > kLaneSamples) SPHRAY_KS(kStatBalanced, 1);
-            if (maxn > 0 && maxn <= kLaneSamples) {
-                double Tl, cr, cg, cb;
-                sample_piece(c, x0, dx, dt, n, 1.0, false, Tl, cr, cg, cb);
-                // exclusive prefix product of the lanes' transmittances
-                double pre = Tl;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const double u = __shfl_up_sync(kFull, pre, o);
-                    if (lane >= o) pre *= u;
-                }
-                double excl = __shfl_up_sync(kFull, pre, 1);
-                if (lane == 0) excl = 1.0;
-                const double Tb = T * excl;  // T before this lane's piece
-                const double Ta = Tb * Tl;   // T after it
-                // early ray termination (raycast.hpp:363, 369): the first piece
-                // that brings T to <= 1e-3 is replayed sample by sample
-                const unsigned failm = __ballot_sync(kFull, n > 0 && !(Ta > 1e-3));
-                const int f = failm ? __ffs(failm) - 1 : 32;
-                const bool inc = lane < f;
-                double rr = inc ? Tb * cr : 0.0, gg = inc ? Tb * cg : 0.0, bb = inc ? Tb * cb : 0.0;
-                double Tend = __shfl_sync(kFull, Ta, 31);
-                if (f < 32) {
-                    double Tr = 0.0, r2 = 0.0, g2 = 0.0, b2 = 0.0;
-                    if (lane == f) {
-                        sample_piece(c, x0, dx, dt, n, Tb, true, Tr, r2, g2, b2);
-                        rr = r2;
-                        gg = g2;
-                        bb = b2;
-                    }
-                    Tend = __shfl_sync(kFull, Tr, f);
-                    term = true;
-                }
-                Cr += rr;
-                Cg += gg;
-                Cb += bb;
-                T = Tend;
-            } else if (maxn > 0) {
-                composite_balanced(n, x0, dx, dt, c);
-            }
-        }
-        // composited start pieces are dead: their slots return to the pool
-        free_slots(have, slot);
-        open_slot = last_slot;
-        open_a0 = last_a0;
-        has_open = true;
+        if (zero && P.tf0_clear) return 0;
+        x0 = fma(lo, P.inv_tau, -static_cast<double>(ts));
+        dx = dt * P.inv_tau;
+        return n;
     }
 
-    // Sample-parallel compositing for chunks containing long pieces: samples
-    // are dealt 32 at a time across the lanes, in order.
-    __device__ void composite_balanced(int n, double x0, double dx, double dt,
-                                       const double (&cl)[D + 1]) {
-        const int incl = warp_incl_scan(n, lane);
-        const int total = __shfl_sync(kFull, incl, 31);
-        for (int base = 0; base < total && !term; base += 32) {
-            const int k = base + lane;
-            const bool act = k < total;
-            int lo_l = 0, hi_l = 31;
-#pragma unroll
-            for (int it = 0; it < 5; ++it) {
-                const int mid = (lo_l + hi_l) >> 1;
-                const int v = __shfl_sync(kFull, incl, mid);
-                if (v > k)
-                    hi_l = mid;
-                else
-                    lo_l = mid + 1;
+    // Samples one piece into a lane's running (T, colour).
+    __device__ __forceinline__ void composite_piece(int64_t ts, int64_t te, const uint64_t (&a)[D + 1],
+                                                    bool stop, double& Tl, double& cr, double& cg,
+                                                    double& cb, int& nsmp) const {
+        double c[D + 1], x0 = 0.0, dx = 0.0, dt = 0.0;
+        const int n = piece_setup(ts, te, a, c, x0, dx, dt);
+        if (n == 0) return;
+        nsmp += n;
+        double To, r, g, b;
+        sample_piece(c, x0, dx, dt, n, Tl, stop, To, r, g, b);
+        cr += r;
+        cg += g;
+        cb += b;
+        Tl = To;
+    }
+
+    // Lane-sequential walk over the sorted flush-set knots [k0, k1) -- the
+    // RayAccumulator recurrence (raycast.hpp:206-244) on one lane: Pc enters
+    // as the sum of every earlier jump around tref, is moved to each knot by
+    // a Taylor shift and takes its jumps; the last knot at a position closes
+    // the piece that starts there, which is composited up to the next knot
+    // (or kept as the open piece when it is the set's last).  `lead`: lane 0
+    // first composites the previous flush's open piece (ot, oa).  stop: the
+    // early-termination replay (absolute T, no side effects).
+    __device__ void walk(int k0, int k1, int nsel, uint64_t (&Pc)[D + 1], bool comp, bool stop,
+                         bool lead, int64_t ot, const uint64_t (&oa)[D + 1], double& Tl, double& cr,
+                         double& cg, double& cb, int& npc, int& nsmp) {
+        if (k0 >= k1) return;
+        int64_t tcur = pool_t(fs[k0]);
+        if (lead && comp) composite_piece(ot, tcur, oa, stop, Tl, cr, cg, cb, nsmp);
+        taylor_shift<D>(Pc, static_cast<uint64_t>(tcur) - static_cast<uint64_t>(tref));
+        int64_t tn = tcur;
+        for (int k = k0; k < k1; ++k) {
+            const int s = fs[k];
+            const int64_t t = tn;
+            if (t != tcur) {
+                taylor_shift<D>(Pc, static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur));
+                tcur = t;
             }
-            const int j = lo_l;
-            const int s = k - (__shfl_sync(kFull, incl, j) - __shfl_sync(kFull, n, j));
-            const double x0_j = __shfl_sync(kFull, x0, j);
-            const double dx_j = __shfl_sync(kFull, dx, j);
-            const double dt_j = __shfl_sync(kFull, dt, j);
-            double c[D + 1];
 #pragma unroll
-            for (int d = 0; d <= D; ++d) c[d] = __shfl_sync(kFull, cl[d], j);
-            double alpha = 0.0, r = 0.0, g = 0.0, b = 0.0;
-            if (act) sample_eval(c, fma(static_cast<double>(s) + 0.5, dx_j, x0_j), dt_j, alpha, r, g, b);
-            const double f = act ? 1.0 - alpha : 1.0;
-            double pre = f;
+            for (int d = 1; d <= D; ++d) Pc[d] += pool_c(d, s);
+            const bool more = k + 1 < nsel;
+            tn = more ? pool_t(fs[k + 1]) : t;
+            if (more && tn == t) continue;  // more jumps at this position
+            ++npc;
+            if (!stop && P.dump_piece_t) {
+                const unsigned long long at = atomicAdd(&P.dump_count[1], 1ull);
+                if (at < P.dump_cap_pieces) {
+                    P.dump_piece_ray[at] = ray_id;
+                    P.dump_piece_t[at] = t;
+#pragma unroll
+                    for (int d = 0; d <= D; ++d) P.dump_piece_a[at * (D + 1) + d] = static_cast<int64_t>(Pc[d]);
+                }
+            }
+            if (!more) {
+                if (!stop) {
+                    w.open[0] = static_cast<uint64_t>(t);
+#pragma unroll
+                    for (int d = 0; d <= D; ++d) w.open[1 + d] = Pc[d];
+                }
+            } else if (comp) {
+                composite_piece(t, tn, Pc, stop, Tl, cr, cg, cb, nsmp);
+            }
+        }
+    }
+
+    // Merge + composite the sorted flush set fs[0, nsel), lane-blocked: lane
+    // l owns the run [l R, l R + R).  (1) each lane sums its jumps shifted to
+    // tref; (2) one exclusive warp scan per order gives every lane the sum of
+    // all earlier jumps (exact modulo 2^64, so equal to RayAccumulator's Int128
+    // result whenever that fits int64); (3) each lane walks its run (walk()),
+    // compositing its pieces from T = 1; (4) one warp combine (prefix product
+    // of the lanes' transmittances) folds the runs into the ray, and the first
+    // lane that brings T to <= 1e-3 replays its run with the reference's
+    // per-sample stop test (raycast.hpp:363, 369).
+    __device__ void merge_composite(int nsel) {
+        const int R = (nsel + 31) >> 5;
+        const int k0 = min(lane * R, nsel), k1 = min(k0 + R, nsel);
+        if (!has_ref) {
+            tref = pool_t(fs[0]);
+            has_ref = true;
+        }
+        uint64_t S[D + 1];
+#pragma unroll
+        for (int d = 0; d <= D; ++d) S[d] = 0ull;
+        for (int k = k0; k < k1; ++k) {
+            const int s = fs[k];
+            uint64_t g[D + 1];
+            g[0] = 0ull;  // b_0 == 0 for every knot
+#pragma unroll
+            for (int d = 1; d <= D; ++d) g[d] = pool_c(d, s);
+            taylor_shift<D>(g, static_cast<uint64_t>(tref) - static_cast<uint64_t>(pool_t(s)));
+#pragma unroll
+            for (int d = 0; d <= D; ++d) S[d] += g[d];
+        }
+        uint64_t E[D + 1];
+#pragma unroll
+        for (int d = 0; d <= D; ++d) {
+            const uint64_t inc = warp_incl_scan(S[d], lane);
+            E[d] = G[d] + (inc - S[d]);
+            G[d] += __shfl_sync(kFull, inc, 31);
+        }
+        const bool lead = lane == 0 && has_open;
+        int64_t ot = 0;
+        uint64_t oa[D + 1];
+#pragma unroll
+        for (int d = 0; d <= D; ++d) oa[d] = 0ull;
+        if (lead) {
+            ot = static_cast<int64_t>(w.open[0]);
+#pragma unroll
+            for (int d = 0; d <= D; ++d) oa[d] = w.open[1 + d];
+        }
+        __syncwarp();
+        const bool comp = !term;
+        double Tl = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
+        int npc = 0, nsmp = 0;
+        uint64_t Pc[D + 1];
+#pragma unroll
+        for (int d = 0; d <= D; ++d) Pc[d] = E[d];
+        walk(k0, k1, nsel, Pc, comp, false, lead, ot, oa, Tl, cr, cg, cb, npc, nsmp);
+        __syncwarp();
+        has_open = true;
+        pieces += __reduce_add_sync(kFull, static_cast<unsigned>(npc));
+        if (SPHRAY_KSTATS) {
+            const unsigned ns = __reduce_add_sync(kFull, static_cast<unsigned>(nsmp));
+            SPHRAY_KS(kStatSamples, ns);
+        }
+        if (comp) {
+            double pre = Tl;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const double u = __shfl_up_sync(kFull, pre, o);
@@ -468,30 +485,45 @@ class RayWorker {
             }
             double excl = __shfl_up_sync(kFull, pre, 1);
             if (lane == 0) excl = 1.0;
-            const double Tb = T * excl;
-            const unsigned okm = __ballot_sync(kFull, act && Tb > 1e-3);
-            const unsigned actm = __ballot_sync(kFull, act);
-            const unsigned fail = actm & ~okm;
-            const int first_fail = fail ? __ffs(fail) - 1 : 32;
-            const bool inc = act && lane < first_fail;
-            const double ta = inc ? Tb * alpha : 0.0;
-            if (inc) {
-                Cr = fma(ta, r, Cr);
-                Cg = fma(ta, g, Cg);
-                Cb = fma(ta, b, Cb);
+            const double Tb = T * excl;  // T before this lane's run
+            const double Ta = Tb * Tl;   // and after it
+            const unsigned failm = __ballot_sync(kFull, nsmp > 0 && !(Ta > 1e-3));
+            const int f = failm ? __ffs(failm) - 1 : 32;
+            if (lane < f) {
+                Cr = fma(Tb, cr, Cr);
+                Cg = fma(Tb, cg, Cg);
+                Cb = fma(Tb, cb, Cb);
             }
-            const unsigned incm = __ballot_sync(kFull, inc);
-            if (incm) T = __shfl_sync(kFull, Tb * f, 31 - __clz(incm));
-            if (fail) term = true;
+            double Tend = __shfl_sync(kFull, Ta, 31);
+            if (f < 32) {
+                double T2 = Tb;
+                if (lane == f) {
+                    double r2 = 0.0, g2 = 0.0, b2 = 0.0;
+                    int d1 = 0, d2 = 0;
+#pragma unroll
+                    for (int d = 0; d <= D; ++d) Pc[d] = E[d];
+                    walk(k0, k1, nsel, Pc, true, true, lead, ot, oa, T2, r2, g2, b2, d1, d2);
+                    Cr += r2;
+                    Cg += g2;
+                    Cb += b2;
+                }
+                Tend = __shfl_sync(kFull, T2, f);
+                term = true;
+            }
+            T = Tend;
         }
+        // every slot of the set is free again: fs sits right above the free
+        // stack (the open piece lives in w.open)
+        nfree += nsel;
+        __syncwarp();
     }
 
     // Sort fs[0, nsel) by knot position: warp LSD radix sort on (t - tmin),
     // 8 bits per pass (flush sets usually span < 2^16 tau: two passes).  The
     // scatter is stable: ranks within a round of 32 come from match.any (a
     // per-bit ballot version measured 2% slower).
-    __device__ void sort_flush_radix(int nsel, int64_t tmin, int bits) {
-        uint16_t* src = w.fs;
+    __device__ void sort_flush_radix(int nsel, uint32_t tmin, int bits) {
+        uint16_t* src = fs;
         uint16_t* dst = w.ps + np;  // free scratch: np + nsel <= cap
 #pragma unroll 1
         for (int shift = 0; shift < bits; shift += 8) {
@@ -500,8 +532,7 @@ class RayWorker {
             __syncwarp();
 #pragma unroll 1
             for (int i = lane; i < nsel; i += 32) {
-                const uint32_t dg = static_cast<uint32_t>(
-                    ((static_cast<uint64_t>(pool_t(src[i])) - static_cast<uint64_t>(tmin)) >> shift) & 255u);
+                const uint32_t dg = ((w.pt[src[i]] - tmin) >> shift) & 255u;
                 atomicAdd(&w.hist[dg], 1u);
             }
             __syncwarp();
@@ -522,9 +553,7 @@ class RayWorker {
                 const int i = c0 + lane;
                 const bool valid = i < nsel;
                 const int sl = valid ? src[i] : 0;
-                const uint32_t dg = valid ? static_cast<uint32_t>(
-                    ((static_cast<uint64_t>(pool_t(sl)) - static_cast<uint64_t>(tmin)) >> shift) & 255u)
-                                          : 0u;
+                const uint32_t dg = valid ? ((w.pt[sl] - tmin) >> shift) & 255u : 0u;
                 const unsigned peers = __match_any_sync(kFull, valid ? dg : 256u + lane);
                 const unsigned below = peers & lanemask_lt();
                 const uint32_t base = valid ? w.hist[dg] : 0u;
@@ -539,27 +568,10 @@ class RayWorker {
             src = dst;
             dst = tmp;
         }
-        if (src != w.fs) {
-            for (int i = lane; i < nsel; i += 32) w.fs[i] = src[i];
+        if (src != fs) {
+            for (int i = lane; i < nsel; i += 32) fs[i] = src[i];
             __syncwarp();
         }
-    }
-
-    __device__ void sort_flush_rank(int nsel) {
-        // ps[np, np + nsel) is free scratch (np + nsel <= cap)
-        for (int i = lane; i < nsel; i += 32) {
-            const int si = w.fs[i];
-            const int64_t ti = pool_t(si);
-            int rank = 0;
-            for (int j = 0; j < nsel; ++j) {
-                const int64_t tj = pool_t(w.fs[j]);
-                rank += (tj < ti) || (tj == ti && j < i);
-            }
-            w.ps[np + rank] = static_cast<uint16_t>(si);
-        }
-        __syncwarp();
-        for (int i = lane; i < nsel; i += 32) w.fs[i] = w.ps[np + i];
-        __syncwarp();
     }
 
     // Finalise every pending knot with t < F (all of them if all_): select
@@ -569,19 +581,24 @@ class RayWorker {
     // equal to RayAccumulator's Int128 result whenever that fits int64).
     __device__ void flush(int64_t F, bool all_) {
         // ---- select t < F into fs, compact the rest of ps in place
+        fs = w.fl + nfree;  // [nfree, nfree + np) is free space above the stack
         int nsel = 0, nkeep = 0;
-        int64_t tmin = INT64_MAX, tmax = INT64_MIN;
+        // F as an offset from tb, clamped to [0, 2^32]
+        const uint64_t dF = static_cast<uint64_t>(F) - static_cast<uint64_t>(tb);
+        const uint64_t Fo = all_ ? 0x100000000ull
+                            : (F <= tb ? 0ull : (dF > 0x100000000ull ? 0x100000000ull : dF));
+        uint32_t tmin = 0xffffffffu, tmax = 0u;
         for (int c0 = 0; c0 < np; c0 += 32) {
             const int i = c0 + lane;
             const bool valid = i < np;
             const int s = valid ? w.ps[i] : 0;
-            const int64_t t = valid ? pool_t(s) : 0;
-            const bool sel = valid && (all_ || t < F);
+            const uint32_t t = valid ? w.pt[s] : 0u;
+            const bool sel = valid && static_cast<uint64_t>(t) < Fo;
             const unsigned msel = __ballot_sync(kFull, sel);
             const unsigned mkeep = __ballot_sync(kFull, valid && !sel);
             __syncwarp();
             if (sel) {
-                w.fs[nsel + __popc(msel & lanemask_lt())] = static_cast<uint16_t>(s);
+                fs[nsel + __popc(msel & lanemask_lt())] = static_cast<uint16_t>(s);
                 tmin = t < tmin ? t : tmin;
                 tmax = t > tmax ? t : tmax;
             } else if (valid) {
@@ -594,70 +611,17 @@ class RayWorker {
         SPHRAY_KS(kStatFlushes, 1);
         SPHRAY_KS(kStatScanned, np);
         SPHRAY_KS(kStatSelected, nsel);
-        SPHRAY_KS(kStatChunks, (nsel + 31) / 32);
         np = nkeep;
         if (SPHRAY_KSTATS && np > max_resid) max_resid = np;
         if (nsel == 0) return;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const int64_t a = __shfl_xor_sync(kFull, tmin, o);
-            const int64_t b = __shfl_xor_sync(kFull, tmax, o);
-            tmin = a < tmin ? a : tmin;
-            tmax = b > tmax ? b : tmax;
-        }
-        const uint64_t range = static_cast<uint64_t>(tmax) - static_cast<uint64_t>(tmin);
-        const int bits = range == 0 ? 0 : 64 - __clzll(static_cast<long long>(range));
-        if (nsel > 1 && bits <= 32)
-            sort_flush_radix(nsel, tmin, bits);
-        else if (nsel > 1)
-            sort_flush_rank(nsel);
+        tmin = __reduce_min_sync(kFull, tmin);
+        tmax = __reduce_max_sync(kFull, tmax);
+        const uint32_t range = tmax - tmin;
+        const int bits = range == 0 ? 0 : 32 - __clz(static_cast<int>(range));
+        if (nsel > 1) sort_flush_radix(nsel, tmin, bits);
 
-        // ---- merge: 32 knots at a time
-        for (int c0 = 0; c0 < nsel; c0 += 32) {
-            const int i = c0 + lane;
-            const bool valid = i < nsel;
-            const int s = valid ? w.fs[i] : 0;
-            const int64_t t = valid ? pool_t(s) : 0;
-            const bool last = valid && ((i == nsel - 1) || (pool_t(w.fs[i + 1]) != t));
-            if (!has_ref) {
-                tref = __shfl_sync(kFull, t, 0);
-                has_ref = true;
-            }
-            uint64_t g[D + 1];
-            g[0] = 0ull;  // b_0 == 0 for every knot
-#pragma unroll
-            for (int d = 1; d <= D; ++d) g[d] = valid ? pool_c(d, s) : 0ull;
-            taylor_shift<D>(g, static_cast<uint64_t>(tref) - static_cast<uint64_t>(t));
-#pragma unroll
-            for (int d = 0; d <= D; ++d) {
-                g[d] = warp_incl_scan(g[d], lane) + G[d];
-                G[d] = __shfl_sync(kFull, g[d], 31);
-            }
-            const unsigned pm = __ballot_sync(kFull, last);
-            const int cp = __popc(pm);
-            if (last) {
-                // the piece at t: a = S(t - tref) G
-                taylor_shift<D>(g, static_cast<uint64_t>(t) - static_cast<uint64_t>(tref));
-#pragma unroll
-                for (int d = 1; d <= D; ++d) pool_c(d, s) = g[d];
-                const int pr = __popc(pm & lanemask_lt());
-                w.pcs[pr] = static_cast<uint16_t>(s);
-                w.na0[pr] = g[0];
-                if (P.dump_piece_t) {
-                    const unsigned long long at = atomicAdd(&P.dump_count[1], 1ull);
-                    if (at < P.dump_cap_pieces) {
-                        P.dump_piece_ray[at] = ray_id;
-                        P.dump_piece_t[at] = t;
-#pragma unroll
-                        for (int d = 0; d <= D; ++d)
-                            P.dump_piece_a[at * (D + 1) + d] = static_cast<int64_t>(g[d]);
-                    }
-                }
-            }
-            pieces += cp;
-            free_slots(valid && !last, s);
-            if (cp > 0) composite_chunk(cp);
-        }
+        merge_composite(nsel);
     }
 
     __device__ void report_overflow(int pi) {
@@ -667,7 +631,7 @@ class RayWorker {
 
     // Quantize the first nq queued hits (lane per hit) and append their knots
     // to the pending list.  Returns false if the window is too small.
-    __device__ bool insert_hits(int nq) {
+    __device__ bool insert_hits(int nq, int64_t F) {
         const bool act = lane < nq;
         int pi = 0;
         double lam = 0.0, tchi = 0.0, h = 0.0;
@@ -692,6 +656,12 @@ class RayWorker {
         if (total == 0) return true;
         if (total > nfree) return false;  // the caller flushed; the window is genuinely full
         const int slot0 = nfree - total + off;  // this lane's slots: fl[slot0 .. slot0 + nk)
+        if (!has_base) {
+            // every knot of the ray is >= the current flush bound
+            tb = F;
+            has_base = true;
+        }
+        bool far_ = false;  // a knot more than 2^32 quanta from tb
         if (emits) {
             double X[3 * D];
             const double* xs = P.xy + static_cast<size_t>(pi) * (3 * D);
@@ -700,13 +670,19 @@ class RayWorker {
             quantize_emit<D, M>(P.Q, X, hp, ovf, [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
                 const int slot = w.fl[slot0 + o];
                 // b[0] is structurally zero (lut.hpp:107-166): only orders 1..D are stored
-                w.pool[slot] = static_cast<uint64_t>(t);
+                const uint64_t to = static_cast<uint64_t>(t) - static_cast<uint64_t>(tb);
+                far_ |= t < tb || to > 0xffffffffull;
+                w.pt[slot] = static_cast<uint32_t>(to);
 #pragma unroll
                 for (int d = 1; d <= D; ++d) pool_c(d, slot) = static_cast<uint64_t>(b[d]);
                 w.ps[np + off + o] = static_cast<uint16_t>(slot);
             });
             if (ovf) report_overflow(pi);
         }
+        // a ray spanning more than 2^32 position quanta does not fit the
+        // 32-bit offsets: treated like a window overflow (retry pass, then
+        // CapacityError)
+        if (__any_sync(kFull, far_)) return false;
         __syncwarp();
         nfree -= total;
         np += total;
@@ -789,7 +765,7 @@ class RayWorker {
                 // at most KN knots); none fitting after a flush = true overflow
                 const int fit = nfree / KN;
                 const int nq = min(min(hq_n, 32), fit);
-                if (nq == 0 || !insert_hits(nq)) return false;
+                if (nq == 0 || !insert_hits(nq, F)) return false;
                 // drop the nq inserted hits (up to 63 queued: shift in chunks)
                 const int rest = hq_n - nq;
                 for (int c0 = 0; c0 < rest; c0 += 32) {
@@ -833,8 +809,7 @@ class RayWorker {
             bool residual = false;  // raycast.hpp:477-480: trailing piece must be zero
             if (knots > 0 && complete && has_open) {
 #pragma unroll
-                for (int d = 1; d <= D; ++d) residual |= pool_c(d, open_slot) != 0;
-                residual |= open_a0 != 0;
+                for (int d = 0; d <= D; ++d) residual |= w.open[1 + d] != 0;
             }
             // RayAccumulator op count for P distinct positions (raycast.hpp:217-244)
             const unsigned long long Pp = pieces;
