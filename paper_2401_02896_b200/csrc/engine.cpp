@@ -303,15 +303,23 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     const int n = static_cast<int>(n_);
     cudaStream_t s = stream_;
 
-    // per-frame uploads: TF (+ segment inverse widths), pow(tau, d) (glibc, quantize.hpp:221)
-    h_tf_.assign(ntf * 6, 0.0);
+    // per-frame uploads: TF (+ per-segment slopes, render_kernel.cuh tf_sample),
+    // pow(tau, d) (glibc, quantize.hpp:221)
+    h_tf_.assign(ntf * kTfPoint, 0.0);
     for (size_t i = 0; i < ntf; ++i) {
-        h_tf_[i * 6 + 0] = tf[i].value;
-        h_tf_[i * 6 + 1] = tf[i].r;
-        h_tf_[i * 6 + 2] = tf[i].g;
-        h_tf_[i * 6 + 3] = tf[i].b;
-        h_tf_[i * 6 + 4] = tf[i].absorption;
-        h_tf_[i * 6 + 5] = i + 1 < ntf ? 1.0 / (tf[i + 1].value - tf[i].value) : 0.0;
+        double* q = &h_tf_[i * kTfPoint];
+        q[0] = tf[i].value;
+        q[1] = tf[i].r;
+        q[2] = tf[i].g;
+        q[3] = tf[i].b;
+        q[4] = tf[i].absorption;
+        if (i + 1 < ntf) {  // d(colour)/d(value) on [value_i, value_i+1]; 0 after the last point
+            const double iw = 1.0 / (tf[i + 1].value - tf[i].value);
+            q[5] = (tf[i + 1].r - tf[i].r) * iw;
+            q[6] = (tf[i + 1].g - tf[i].g) * iw;
+            q[7] = (tf[i + 1].b - tf[i].b) * iw;
+            q[8] = (tf[i + 1].absorption - tf[i].absorption) * iw;
+        }
     }
     d_tf_.ensure(h_tf_.size() * sizeof(double));
     CUDA_OK(cudaMemcpyAsync(d_tf_.p, h_tf_.data(), h_tf_.size() * sizeof(double), cudaMemcpyHostToDevice, s));
@@ -483,7 +491,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     // bound the resident warps; the default window is the largest of a few
     // sizes that reaches the best warps/SM (windows below ~384 slots make
     // config-3 rays overflow into the retry pass).
-    const size_t tfb_full = ntf * 6 * sizeof(double);
+    const size_t tfb_full = ntf * kTfPoint * sizeof(double);
     const size_t tfb = (tfb_full <= 4096 && !std::getenv("SPHRAY_TF_GLOBAL")) ? tfb_full : 0;
     P.tf_smem = static_cast<int>(tfb);
     auto best_shape = [&](int cap_, int& warps_, int& bps_) {

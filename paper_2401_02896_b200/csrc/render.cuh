@@ -14,6 +14,7 @@ constexpr int kTileShift = 3;  // 8x8-pixel screen tiles
 constexpr int kTile = 1 << kTileShift;
 constexpr int kTileRays = kTile * kTile;
 constexpr int kHitQueue = 64;
+constexpr int kTfPoint = 10;  // doubles per transfer-function point on the device
 constexpr int kMaxJ = kMaxM * kMaxDegree;
 
 #ifdef __CUDACC__
@@ -67,7 +68,7 @@ struct FrameParams {
     double inv_tau;   // 1 / tau for sample abscissae (compositing only)
     double inv_step;  // 1 / step (sample counts, checked against the exact quotient)
     // transfer function (raycast.hpp:313-338)
-    const double* tf;  // ntf * 6: value, r, g, b, absorption, 1/(next value - value)
+    const double* tf;  // ntf * kTfPoint: value, r, g, b, absorption, 4 slopes to the next point, pad
     int ntf;
     int tf0_clear;  // tf.sample(0).absorption == 0: zero pieces are exact no-ops
     double step;

@@ -74,11 +74,13 @@ __device__ __forceinline__ int64_t knot_floor(float front, double tau) {
     return static_cast<int64_t>(v);
 }
 
-// TransferFunction::sample (raycast.hpp:326-337).  The device TF holds 6
-// doubles per point: value, r, g, b, absorption, 1/(next value - value), so
-// the interpolation weight (v - a.value)/(b.value - a.value) is one multiply
-// (<= 1 ulp from the reference's division; inside the RGB tolerance).
-constexpr int kTfStride = 6;
+// TransferFunction::sample (raycast.hpp:326-337).  The device TF holds
+// kTfPoint doubles per point: value, r, g, b, absorption and the four slopes
+// to the next point, so the interpolation is one fma per channel,
+// c_a + (v - value_a) * slope_a (within a few ulps of the reference's
+// c_a + t (c_b - c_a); inside the RGB tolerance).  Clamping uses w = 0,
+// which reproduces the end point exactly.
+constexpr int kTfStride = kTfPoint;
 
 // TF readers: the per-CTA shared copy (ld.shared) or global memory.
 struct TfShared {
@@ -97,29 +99,20 @@ struct TfGlobal {
 template <class Ld>
 __device__ __forceinline__ void tf_sample(const Ld& ld, int n, double v, double& r, double& g,
                                           double& b, double& ab) {
-    if (v <= ld(0)) {
-        r = ld(1);
-        g = ld(2);
-        b = ld(3);
-        ab = ld(4);
-        return;
-    }
     const int last = kTfStride * (n - 1);
-    if (v >= ld(last)) {
-        r = ld(last + 1);
-        g = ld(last + 2);
-        b = ld(last + 3);
-        ab = ld(last + 4);
-        return;
+    const bool lo = v <= ld(0), hi = v >= ld(last);
+    int a = 0;
+    if (!lo && !hi) {
+        int i = kTfStride;
+        while (ld(i) < v) i += kTfStride;
+        a = i - kTfStride;
     }
-    int i = kTfStride;
-    while (ld(i) < v) i += kTfStride;
-    const int A = i - kTfStride;
-    const double w = (v - ld(A)) * ld(A + 5);
-    r = fma(w, ld(i + 1) - ld(A + 1), ld(A + 1));
-    g = fma(w, ld(i + 2) - ld(A + 2), ld(A + 2));
-    b = fma(w, ld(i + 3) - ld(A + 3), ld(A + 3));
-    ab = fma(w, ld(i + 4) - ld(A + 4), ld(A + 4));
+    if (hi) a = last;
+    const double w = (lo || hi) ? 0.0 : v - ld(a);
+    r = fma(w, ld(a + 5), ld(a + 1));
+    g = fma(w, ld(a + 6), ld(a + 2));
+    b = fma(w, ld(a + 7), ld(a + 3));
+    ab = fma(w, ld(a + 8), ld(a + 4));
 }
 
 // n = max(2, ceil((hi - lo) / step)) exactly as the reference counts samples
