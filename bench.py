@@ -117,6 +117,20 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def measured_traffic(config, res, world):
+    """DRAM bytes (read + write) of one main render launch on this workload,
+    from the committed ncu capture (profiles/r01_render_traffic.json, made by
+    scripts/gpu_round.sh); None when absent or for another workload."""
+    path = os.path.join(ROOT, "profiles", "r01_render_traffic.json")
+    try:
+        d = json.load(open(path))
+    except (OSError, ValueError):
+        return None
+    if d.get("config") != config or d.get("res") != res or d.get("world", 1) != world:
+        return None
+    return d
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -310,9 +324,13 @@ def run_ours(args):
     alg_bytes = (len(ps) * per_particle + st.candidates * (4 + 8) +
                  res * res * 3 * 8 / max(world, 1))
     achieved = alg_bytes / (render_ms * 1e-3) / 1e9
+    traffic = measured_traffic(args.config, res, world)
     roof = {"bound": "hbm", "kernel": "k_render_rays", "achieved": achieved,
             "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-            "frac": achieved / peaks.get("hbm_gbs", 6650.0), "traffic": None,
+            "frac": achieved / peaks.get("hbm_gbs", 6650.0),
+            "traffic": traffic["dram_bytes"] if traffic else None,
+            "traffic_source": traffic["source"] if traffic else None,
+            "algorithmic_bytes": alg_bytes,
             "peak_source": peak_src,
             "note": "the render kernel is ALU/FP64 issue-bound, not HBM-bound (SURVEY.md 8(d)); "
                     "achieved = compulsory bytes (particle records + candidate list + image) "
