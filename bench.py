@@ -335,6 +335,21 @@ def run_ours(args):
             "note": "the render kernel is ALU/FP64 issue-bound, not HBM-bound (SURVEY.md 8(d)); "
                     "achieved = compulsory bytes (particle records + candidate list + image) "
                     "/ median render-kernel time"}
+    # second roofline: the merge against the measured int64
+    # multiply/add issue peak of this GPU; algorithmic ops = the reference's
+    # RayAccumulator op count (RenderStats.int_ops, raycast.hpp:217-244)
+    alu = None
+    try:
+        pk = S.probe_alu_peaks(local)
+        ach = st.int_ops / (render_ms * 1e-3) / 1e9
+        alu = {"bound": "alu", "kernel": "k_render_rays (merge)", "unit": "Gop/s",
+               "achieved": ach, "peak": pk["int64_gops"], "frac": ach / pk["int64_gops"],
+               "fp64_peak_gflops": pk["fp64_gflops"],
+               "note": "achieved = RenderStats.int_ops (int64 mul/add of the reference's "
+                       "sequential merge) / median render-kernel time; peak = measured int64 "
+                       "mul+add issue rate (sphray_probe_alu_peaks)"}
+    except Exception as e:  # report, never fake
+        alu = {"bound": "alu", "unavailable": str(e)}
 
     if rank == 0:
         cpu = None
@@ -358,6 +373,7 @@ def run_ours(args):
                                       "particles replicated, NCCL tile gather",
                        "l2": "256 MB buffer written between frames (> 126 MB L2)"},
             "roofline": roof,
+            "alu_roofline": alu,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(st.launches) * args.steps,

@@ -147,6 +147,13 @@ const char* sphray_build_info(void);
 sphray_status sphray_context_create(int device, sphray_context** out, sphray_error* err);
 void sphray_context_destroy(sphray_context* ctx);
 
+/* Diagnostics (no reference counterpart): measured ALU issue peaks of a
+ * device -- int64 multiply/add operations per second and fp64 flops per
+ * second, in units of 1e9 -- the denominators of the benchmark's ALU
+ * roofline for the merge. */
+sphray_status sphray_probe_alu_peaks(int device, double* int64_gops, double* fp64_gflops,
+                                     sphray_error* err);
+
 /* Multi-GPU (one process per GPU): `unique_id` is 128 bytes produced by
  * sphray_comm_unique_id on rank 0 and broadcast by the caller.  Image tiles are
  * interleaved over ranks; finished tiles are gathered with NCCL over NVLink. */

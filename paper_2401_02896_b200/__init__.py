@@ -159,6 +159,7 @@ def load_library():
     L.sphray_build_info.restype = C.c_char_p
     L.sphray_context_create.argtypes = [C.c_int, P(C.c_void_p), P(_Error)]
     L.sphray_context_destroy.argtypes = [C.c_void_p]
+    L.sphray_probe_alu_peaks.argtypes = [C.c_int, P(C.c_double), P(C.c_double), P(_Error)]
     L.sphray_comm_unique_id.argtypes = [C.c_char_p, P(_Error)]
     L.sphray_context_init_comm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p, P(_Error)]
     L.sphray_context_set_shard.argtypes = [C.c_void_p, C.c_int, C.c_int, P(_Error)]
@@ -420,6 +421,14 @@ def choose_quanta(lut: Lut, stats: DatasetStats, width: int = 64,
     _check(L.sphray_choose_quanta(C.byref(lut.view), C.byref(ds), int(width), kappa, kappa_prime,
                                   C.byref(out), C.byref(err)), err)
     return QuantaConfig(out.tau, out.sigma, out.int_width)
+
+
+def probe_alu_peaks(device: int = 0) -> dict:
+    """Measured int64 multiply/add and fp64 FMA issue peaks of `device`."""
+    L = load_library()
+    gi, gf, err = C.c_double(), C.c_double(), _Error()
+    _check(L.sphray_probe_alu_peaks(device, C.byref(gi), C.byref(gf), C.byref(err)), err)
+    return {"int64_gops": gi.value, "fp64_gflops": gf.value}
 
 
 def generate_scene(config: int, n: int = 0, seed: Optional[int] = None) -> np.ndarray:

@@ -96,6 +96,14 @@ sphray_status sphray_context_create(int device, sphray_context** out, sphray_err
 
 void sphray_context_destroy(sphray_context* ctx) { delete ctx; }
 
+sphray_status sphray_probe_alu_peaks(int device, double* int64_gops, double* fp64_gflops,
+                                     sphray_error* err) {
+    return guarded(err, [&] {
+        if (!int64_gops || !fp64_gflops) fail(SPHRAY_ERR_CONFIG, "null output pointer");
+        probe_alu_peaks(device, int64_gops, fp64_gflops);
+    });
+}
+
 sphray_status sphray_comm_unique_id(uint8_t unique_id[128], sphray_error* err) {
     return guarded(err, [&] { comm_unique_id(unique_id); });
 }

@@ -642,7 +642,9 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     if (trace.on && (st[kStatFlushes] | st[kStatBatches])) {
         static const char* names[] = {"flushes", "scanned", "selected", "chunks", "radix_passes",
                                       "batches", "samples", "balanced", "gather", "resid<128",
-                                      "resid<192", "resid<256", "resid<320", "resid<384", "resid>=384"};
+                                      "resid<192", "resid<256", "resid<320", "resid<384", "resid>=384",
+                                      "bits<=8", "bits<=10", "bits<=12", "bits<=14", "bits<=16",
+                                      "bits>16"};
         for (int k = kStatFirstK; k < kStatCount; ++k)
             trace.line += std::string(" ") + names[k - kStatFirstK] + "=" + std::to_string(st[k]);
     }

@@ -72,6 +72,9 @@ struct LutHost {
 };
 
 LutHost make_lut(const sphray_lut_view& v);
+
+// probe.cu: measured issue peaks (int64 mul/add ops/s, fp64 flops/s) of this GPU
+void probe_alu_peaks(int device, double* int64_gops, double* fp64_gflops);
 void validate_approx(int K, int D);  // ApproxConfig::validate approx.hpp:27-30
 
 // ---------------------------------------------------------------------------

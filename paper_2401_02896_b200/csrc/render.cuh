@@ -120,7 +120,8 @@ enum StatIndex {
     kStatBalanced = 15,  // chunks sent to the sample-parallel path
     kStatGather = 16,    // 32-candidate gather iterations
     kStatPeak0 = 17,     // rays by largest post-flush residual: <128, <192, <256, <320, <384, >=384
-    kStatCount = 23
+    kStatBits0 = 23,     // flushes by sort-key bits: <=8, <=10, <=12, <=14, <=16, >16
+    kStatCount = 29
 };
 constexpr int kStatFirstK = kStatFlushes;
 

@@ -120,6 +120,7 @@ __device__ __forceinline__ void tf_sample(const Ld& ld, int n, double v, double&
 // the quotient is within rounding distance of an integer.
 __device__ __forceinline__ int sample_count(double len, double step, double inv_step) {
     const double q = len * inv_step;
+    if (q < 1.9) return 2;  // len/step < 2 for sure: the common case
     double c = ceil(q);
     if (fabs(q - rint(q)) <= 1e-12 * q + 1e-300) c = ceil(div_exact(len, step));
     return c > 2.0 ? static_cast<int>(c) : 2;
@@ -629,6 +630,10 @@ class RayWorker {
         tmax = __reduce_max_sync(kFull, tmax);
         const uint32_t range = tmax - tmin;
         const int bits = range == 0 ? 0 : 32 - __clz(static_cast<int>(range));
+        if (SPHRAY_KSTATS) {
+            const int bb = bits <= 8 ? 0 : bits <= 10 ? 1 : bits <= 12 ? 2 : bits <= 14 ? 3 : bits <= 16 ? 4 : 5;
+            SPHRAY_KS(kStatBits0 + bb, 1);
+        }
         if (nsel > 1) sort_flush_radix(nsel, tmin, bits);
 
         merge_composite(nsel);
