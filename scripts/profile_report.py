@@ -20,11 +20,22 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 
+_SCALE = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3,  # -> ms
+          "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}                 # -> bytes
+
+
 def raw_metrics(rep):
+    """name -> value, with durations in ms and byte counts in bytes."""
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
-    return dict(zip(rows[0], rows[2]))
+    out = {}
+    for name, unit, val in zip(rows[0], rows[1], rows[2]):
+        try:
+            out[name] = str(float(val.replace(",", "")) * _SCALE.get(unit, 1.0))
+        except ValueError:
+            out[name] = val
+    return out
 
 
 def fnum(d, k):
@@ -65,7 +76,7 @@ def main():
     if a.rep:
         d = raw_metrics(a.rep)
         keys = [
-            ("duration (ms)", "gpu__time_duration.sum", 1e-6),
+            ("duration (ms)", "gpu__time_duration.sum", 1),
             ("SM cycles", "sm__cycles_elapsed.avg", 1),
             ("warp instructions executed", "smsp__inst_executed.sum", 1),
             ("IPC per SM (of 4)", "sm__inst_executed.avg.per_cycle_active", 1),
