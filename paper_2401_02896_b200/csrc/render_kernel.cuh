@@ -23,6 +23,9 @@
 #include "quantize.cuh"
 #include "render.cuh"
 
+#ifndef SPHRAY_FLUSH_AT
+#define SPHRAY_FLUSH_AT 4  // flush once the pending list holds SPHRAY_FLUSH_AT/8 of the window
+#endif
 #ifndef SPHRAY_KSTATS
 #define SPHRAY_KSTATS 0
 #endif
@@ -388,15 +391,7 @@ class RayWorker {
             tn = more ? pool_t(fs[k + 1]) : t;
             if (more && tn == t) continue;  // more jumps at this position
             ++npc;
-            if (!stop && P.dump_piece_t) {
-                const unsigned long long at = atomicAdd(&P.dump_count[1], 1ull);
-                if (at < P.dump_cap_pieces) {
-                    P.dump_piece_ray[at] = ray_id;
-                    P.dump_piece_t[at] = t;
-#pragma unroll
-                    for (int d = 0; d <= D; ++d) P.dump_piece_a[at * (D + 1) + d] = static_cast<int64_t>(Pc[d]);
-                }
-            }
+            if (!stop && P.dump_piece_t) dump_piece(t, Pc);
             if (!more) {
                 if (!stop) {
                     w.open[0] = static_cast<uint64_t>(t);
@@ -406,6 +401,17 @@ class RayWorker {
             } else if (comp) {
                 composite_piece(t, tn, Pc, stop, Tl, cr, cg, cb, nsmp);
             }
+        }
+    }
+
+    // validation dump of one FieldPiece
+    __device__ __forceinline__ void dump_piece(int64_t t, const uint64_t (&a)[D + 1]) const {
+        const unsigned long long at = atomicAdd(&P.dump_count[1], 1ull);
+        if (at < P.dump_cap_pieces) {
+            P.dump_piece_ray[at] = ray_id;
+            P.dump_piece_t[at] = t;
+#pragma unroll
+            for (int d = 0; d <= D; ++d) P.dump_piece_a[at * (D + 1) + d] = static_cast<int64_t>(a[d]);
         }
     }
 
@@ -706,6 +712,29 @@ class RayWorker {
         return true;
     }
 
+    // Drop the first nq queued hits (up to 63 queued: shift in chunks of 32).
+    __device__ __forceinline__ void drop_queued(int nq, int& hq_n) {
+        const int rest = hq_n - nq;
+        for (int c0 = 0; c0 < rest; c0 += 32) {
+            const int i = c0 + lane;
+            int32_t qp = 0;
+            double ql = 0.0, qt = 0.0;
+            if (i < rest) {
+                qp = w.hq_p[nq + i];
+                ql = w.hq_d2[nq + i];
+                qt = w.hq_t[nq + i];
+            }
+            __syncwarp();
+            if (i < rest) {
+                w.hq_p[i] = qp;
+                w.hq_d2[i] = ql;
+                w.hq_t[i] = qt;
+            }
+            __syncwarp();
+        }
+        hq_n = rest;
+    }
+
     // One ray; returns false if the knot window overflowed (ray is retried).
     __device__ bool run(int px, int py) {
         reset();
@@ -760,48 +789,33 @@ class RayWorker {
                 cursor += 32;
             }
             __syncwarp();
-            // ---- flush: every knot below F is final.  F bounds every knot of
-            // the queued hits and of the untested candidates (depth-sorted).
-            // One call site keeps the kernel's code (and its i-cache
-            // footprint) small.
+            // ---- insert as many queued hits as the window surely takes (each
+            // emits at most KN knots), then flush: every knot below F -- the
+            // bound of the first hit still queued, or of the next untested
+            // candidate (both depth-sorted) -- is final.
+            bool stuck = false;
+            if (hq_n > 0) {
+                const int nq = min(min(hq_n, 32), nfree / KN);
+                if (nq == 0) {
+                    stuck = true;
+                } else {
+                    if (!insert_hits(nq, knot_floor(P.front[w.hq_p[0]], P.Q.tau))) return false;
+                    drop_queued(nq, hq_n);
+                }
+            }
             const bool final_ = hq_n == 0 && cursor >= ce;
             int64_t F = INT64_MAX;
             if (!final_) {
-                // candidates and queued hits are in front order: the first
-                // unprocessed one bounds every knot still to come
                 const uint32_t pn = hq_n > 0 ? static_cast<uint32_t>(w.hq_p[0]) : P.cand[cursor];
                 F = knot_floor(P.front[pn], P.Q.tau);
             }
-            if (final_ || nfree < 32 * KN || np >= (P.cap >> 1)) flush(F, final_);
+            if (final_ || stuck || nfree < 32 * KN || np >= (P.cap * SPHRAY_FLUSH_AT) / 8) {
+                const int np0 = np;
+                flush(F, final_);
+                if (stuck && np == np0) return false;  // nothing final: the window is too small
+            }
             if (final_) break;
             if (term && P.mode == SPHRAY_MODE_FAST) break;
-            if (hq_n > 0) {
-                // as many queued hits as the window can surely take (each emits
-                // at most KN knots); none fitting after a flush = true overflow
-                const int fit = nfree / KN;
-                const int nq = min(min(hq_n, 32), fit);
-                if (nq == 0 || !insert_hits(nq, F)) return false;
-                // drop the nq inserted hits (up to 63 queued: shift in chunks)
-                const int rest = hq_n - nq;
-                for (int c0 = 0; c0 < rest; c0 += 32) {
-                    const int i = c0 + lane;
-                    int32_t qp = 0;
-                    double ql = 0.0, qt = 0.0;
-                    if (i < rest) {
-                        qp = w.hq_p[nq + i];
-                        ql = w.hq_d2[nq + i];
-                        qt = w.hq_t[nq + i];
-                    }
-                    __syncwarp();
-                    if (i < rest) {
-                        w.hq_p[i] = qp;
-                        w.hq_d2[i] = ql;
-                        w.hq_t[i] = qt;
-                    }
-                    __syncwarp();
-                }
-                hq_n = rest;
-            }
         }
         return true;
     }
