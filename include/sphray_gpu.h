@@ -235,6 +235,11 @@ sphray_status sphray_quantize_hits(sphray_context* ctx, const sphray_particle* p
 sphray_status sphray_compute_dataset_stats(const sphray_particle* particles, size_t n,
                                            const sphray_lut_view* lut, double clustering_factor,
                                            sphray_dataset_stats* out, sphray_error* err);
+/* dataset_stats (quantize.hpp:129-165) of the scene resident in `ctx`
+ * (sphray_scene_upload), on the GPU: radix-sorted medians and a max
+ * reduction -- bit-identical to sphray_compute_dataset_stats. */
+sphray_status sphray_scene_dataset_stats(sphray_context* ctx, double clustering_factor,
+                                         sphray_dataset_stats* out, sphray_error* err);
 sphray_status sphray_choose_quanta(const sphray_lut_view* lut, const sphray_dataset_stats* ds,
                                    int int_width, double kappa, double kappa_prime,
                                    sphray_quanta* out, sphray_error* err);

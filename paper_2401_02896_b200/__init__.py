@@ -186,6 +186,7 @@ def load_library():
                                        P(C.c_int64), P(C.c_int32), P(_Error)]
     L.sphray_compute_dataset_stats.argtypes = [P(_Particle), C.c_size_t, P(_LutView), C.c_double,
                                                P(_DStats), P(_Error)]
+    L.sphray_scene_dataset_stats.argtypes = [C.c_void_p, C.c_double, P(_DStats), P(_Error)]
     L.sphray_choose_quanta.argtypes = [P(_LutView), P(_DStats), C.c_int, C.c_double, C.c_double,
                                        P(_Quanta), P(_Error)]
     L.sphray_lut_parse.argtypes = [C.c_void_p, C.c_size_t, P(_LutView), C.c_char_p, P(_Error)]
@@ -563,6 +564,13 @@ class Context:
                                            P(pa, C.c_int64), len(rays), len(pt), C.byref(nr),
                                            C.byref(npc), C.byref(err)), err)
         return dict(rays=rays, piece_off=off, piece_t=pt, piece_a=pa)
+
+    def dataset_stats(self, clustering_factor: float = 16.0) -> DatasetStats:
+        """dataset_stats (quantize.hpp:129-165) of the uploaded scene, on the GPU."""
+        out, err = _DStats(), _Error()
+        _check(self._L.sphray_scene_dataset_stats(self._h, clustering_factor, C.byref(out),
+                                                  C.byref(err)), err)
+        return DatasetStats._from(out)
 
     def quantize_hits(self, particles, t_chi, lam, lut: Lut, qc: QuantaConfig):
         """quantize_particle (quantize.hpp:199-250) for explicit hits (one particle row each)."""

@@ -269,6 +269,14 @@ sphray_status sphray_compute_dataset_stats(const sphray_particle* particles, siz
     });
 }
 
+sphray_status sphray_scene_dataset_stats(sphray_context* ctx, double clustering_factor,
+                                         sphray_dataset_stats* out, sphray_error* err) {
+    return guarded(err, [&] {
+        if (!ctx || !out) fail(SPHRAY_ERR_CONFIG, "null context/output");
+        *out = ctx->engine->scene_dataset_stats(clustering_factor);
+    });
+}
+
 sphray_status sphray_choose_quanta(const sphray_lut_view* lut, const sphray_dataset_stats* ds,
                                    int int_width, double kappa, double kappa_prime,
                                    sphray_quanta* out, sphray_error* err) {

@@ -279,6 +279,30 @@ struct Trace {
 };
 }  // namespace
 
+sphray_dataset_stats Engine::scene_dataset_stats(double clustering_factor) {
+    set_device();
+    if (!has_scene_) fail(SPHRAY_ERR_CONFIG, "no scene uploaded");
+    if (n_ == 0) fail(SPHRAY_ERR_CONFIG, "dataset_stats: empty particle set");
+    if (!(clustering_factor > 0.0))
+        fail(SPHRAY_ERR_CONFIG, "dataset_stats: clustering factor must be positive");
+    double med[4], phi_max = 0.0;
+    bool bad = false;
+    device_dataset_stats(d_pxyzh_.as<double4>(), d_mvr_.as<double4>(), n_, stream_, med, &phi_max, &bad);
+    if (bad) fail(SPHRAY_ERR_CONFIG, "dataset_stats: particles need positive smoothing radius and density");
+    sphray_dataset_stats st{};
+    st.mass_r = med[0];
+    st.density_r = med[1];
+    st.h_r = med[2];
+    st.value_r = med[3];
+    st.phi_repr = st.mass_r * st.value_r / (st.density_r * st.h_r * st.h_r * st.h_r);
+    st.clustering_factor = clustering_factor;
+    st.count = n_;
+    double amp = 0.0;
+    for (int e = 0; e < lut_.N; ++e) amp = std::max(amp, entry_amplitude(lut_, e));
+    st.a_max = clustering_factor * phi_max * amp;
+    return st;
+}
+
 void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t ntf,
                     const sphray_quanta& qc, const sphray_dataset_stats& ds,
                     const sphray_render_options& opts, double* rgb_host,

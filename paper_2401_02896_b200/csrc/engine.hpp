@@ -55,6 +55,8 @@ class Engine {
     void init_comm(int rank, int nranks, const uint8_t id[128]);
     void set_shard(int rank, int nranks);
     void upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_view& lut);
+    // dataset_stats (quantize.hpp:129-165) of the uploaded scene, computed on the GPU
+    sphray_dataset_stats scene_dataset_stats(double clustering_factor);
     // Renders the resident scene.  rgb_host may be null (image stays on device).
     void render(const sphray_camera& cam, const sphray_tf_point* tf, size_t ntf,
                 const sphray_quanta& qc, const sphray_dataset_stats& ds,

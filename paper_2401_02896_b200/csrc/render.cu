@@ -20,6 +20,8 @@
 
 #include <cub/cub.cuh>
 
+#include <cstring>
+
 #include "device_math.cuh"
 #include "render.cuh"
 
@@ -182,6 +184,41 @@ __global__ void k_scatter_scene(const sphray_particle* ps, const double* powh_in
     mvr[i] = make_double4(p.mass, p.value, p.density, 0.0);
     for (int d = 0; d < D; ++d) powh[i * D + d] = powh_in[static_cast<size_t>(s) * D + d];
     orig[i] = static_cast<int32_t>(s);
+}
+
+// dataset_stats (quantize.hpp:129-165) on the resident scene: the four
+// property columns for the medians, phi_max = max |(m v) / (((rho h) h) h)|
+// in the reference's operation order, and the positivity check of h, rho.
+__global__ void k_stats_columns(const double4* pxyzh, const double4* mvr, size_t n, double* mass,
+                                double* density, double* h, double* value,
+                                unsigned long long* phi_bits, unsigned int* bad) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    unsigned long long best = 0ull;
+    bool b = false;
+    if (i < n) {
+        const double4 p = pxyzh[i];
+        const double4 q = mvr[i];
+        mass[i] = q.x;
+        value[i] = q.y;
+        density[i] = q.z;
+        h[i] = p.w;
+        b = !(p.w > 0.0) || !(q.z > 0.0);
+        // p.mass * p.value / (p.density * p.h * p.h * p.h)   (host.cpp / quantize.hpp:141)
+        const double num = __dmul_rn(q.x, q.y);
+        const double den = __dmul_rn(__dmul_rn(__dmul_rn(q.z, p.w), p.w), p.w);
+        const double phi = fabs(__ddiv_rn(num, den));
+        best = phi == phi ? __double_as_longlong(phi) : 0ull;  // |phi| >= 0: bits order = value order
+    }
+    // warp max, one atomic per warp
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long u = __shfl_xor_sync(0xffffffffu, best, o);
+        best = u > best ? u : best;
+    }
+    const unsigned any_bad = __ballot_sync(0xffffffffu, b);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(phi_bits, best);
+        if (any_bad) atomicOr(bad, 1u);
+    }
 }
 
 }  // namespace
@@ -360,6 +397,56 @@ void cub_sort(const unsigned long long* kin, unsigned long long* kout, const uin
     if (n == 0) return;
     SPHRAY_CUDA_OK(cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout,
                                                    static_cast<int64_t>(n), 0, end_bit, s));
+}
+
+namespace {
+struct Scratch {  // RAII device scratch for the one-off statistics pass
+    void* p = nullptr;
+    explicit Scratch(size_t b) {
+        if (cudaMalloc(&p, b ? b : 1) != cudaSuccess) fail(SPHRAY_ERR_CUDA, "dataset_stats: cudaMalloc failed");
+    }
+    ~Scratch() { cudaFree(p); }
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+};
+}  // namespace
+
+void device_dataset_stats(const double4* pxyzh, const double4* mvr, size_t n, cudaStream_t s,
+                          double med[4], double* phi_max, bool* bad) {
+    Scratch cols(n * 4 * sizeof(double)), sorted(n * sizeof(double)), small(16);
+    double* c = static_cast<double*>(cols.p);
+    unsigned long long* pb = static_cast<unsigned long long*>(small.p);
+    SPHRAY_CUDA_OK(cudaMemsetAsync(small.p, 0, 16, s));
+    k_stats_columns<<<grid_for(n, 256), 256, 0, s>>>(pxyzh, mvr, n, c, c + n, c + 2 * n, c + 3 * n, pb,
+                                                     reinterpret_cast<unsigned int*>(pb + 1));
+    SPHRAY_CUDA_OK(cudaGetLastError());
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, bytes, static_cast<const double*>(nullptr),
+                                   static_cast<double*>(nullptr), static_cast<int64_t>(n), 0,
+                                   static_cast<int>(sizeof(double) * 8), s);
+    Scratch tmp(bytes);
+    double* out = static_cast<double*>(sorted.p);
+    for (int k = 0; k < 4; ++k) {
+        // medians of sorted columns (detail::median, quantize.hpp:118-122); the
+        // radix order equals std::sort's except for the relative order of -0.0
+        // and +0.0, which compare equal
+        SPHRAY_CUDA_OK(cub::DeviceRadixSort::SortKeys(tmp.p, bytes, c + k * n, out,
+                                                      static_cast<int64_t>(n), 0,
+                                                      static_cast<int>(sizeof(double) * 8), s));
+        double mid[2] = {0.0, 0.0};
+        const size_t a = n % 2 ? n / 2 : n / 2 - 1;
+        SPHRAY_CUDA_OK(cudaMemcpyAsync(mid, out + a, (n % 2 ? 1 : 2) * sizeof(double),
+                                       cudaMemcpyDeviceToHost, s));
+        SPHRAY_CUDA_OK(cudaStreamSynchronize(s));
+        med[k] = n % 2 ? mid[0] : 0.5 * (mid[0] + mid[1]);
+    }
+    unsigned long long hb[2] = {0, 0};
+    SPHRAY_CUDA_OK(cudaMemcpyAsync(hb, small.p, 16, cudaMemcpyDeviceToHost, s));
+    SPHRAY_CUDA_OK(cudaStreamSynchronize(s));
+    double pm;
+    std::memcpy(&pm, &hb[0], sizeof(pm));
+    *phi_max = pm;
+    *bad = (hb[1] & 0xffffffffull) != 0;
 }
 
 }  // namespace sphray_b200

@@ -144,6 +144,11 @@ struct PrepParams {
 
 size_t warp_smem_bytes(int D, int cap, int m);
 int max_blocks_per_sm(int D, int m, int warps, size_t smem);
+// dataset_stats (quantize.hpp:129-165) of the resident scene: medians of
+// mass, density, h, value (med[0..3]), phi_max, and whether some particle has
+// h <= 0 or density <= 0.
+void device_dataset_stats(const double4* pxyzh, const double4* mvr, size_t n, cudaStream_t s,
+                          double med[4], double* phi_max, bool* bad);
 void launch_render(const FrameParams& P, int D, int m, int blocks, int warps, cudaStream_t s);
 void launch_prep(const PrepParams& p, cudaStream_t s);
 void launch_emit(const PrepParams& p, const uint32_t* offsets, unsigned long long* keys,

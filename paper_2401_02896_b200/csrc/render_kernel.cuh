@@ -23,6 +23,12 @@
 #include "quantize.cuh"
 #include "render.cuh"
 
+#ifndef SPHRAY_GATHER_TO
+#define SPHRAY_GATHER_TO 32  // hits queued before an insert/flush step (<= kHitQueue)
+#endif
+#ifndef SPHRAY_INSERT_ROUNDS
+#define SPHRAY_INSERT_ROUNDS 1  // 32-hit insert rounds per step
+#endif
 #ifndef SPHRAY_FLUSH_AT
 #define SPHRAY_FLUSH_AT 4  // flush once the pending list holds SPHRAY_FLUSH_AT/8 of the window
 #endif
@@ -747,7 +753,7 @@ class RayWorker {
         int hq_n = 0;
         while (true) {
             // ---- gather: exact hit test of 32 candidates at a time
-            while (hq_n < 32 && cursor < ce) {
+            while (hq_n < SPHRAY_GATHER_TO && hq_n <= kHitQueue - 32 && cursor < ce) {
                 SPHRAY_KS(kStatGather, 1);
                 const uint32_t c = cursor + lane;
                 bool hit = false;
@@ -794,14 +800,15 @@ class RayWorker {
             // bound of the first hit still queued, or of the next untested
             // candidate (both depth-sorted) -- is final.
             bool stuck = false;
-            if (hq_n > 0) {
+#pragma unroll 1
+            for (int round = 0; round < SPHRAY_INSERT_ROUNDS && hq_n > 0; ++round) {
                 const int nq = min(min(hq_n, 32), nfree / KN);
                 if (nq == 0) {
-                    stuck = true;
-                } else {
-                    if (!insert_hits(nq, knot_floor(P.front[w.hq_p[0]], P.Q.tau))) return false;
-                    drop_queued(nq, hq_n);
+                    stuck = round == 0;
+                    break;
                 }
+                if (!insert_hits(nq, knot_floor(P.front[w.hq_p[0]], P.Q.tau))) return false;
+                drop_queued(nq, hq_n);
             }
             const bool final_ = hq_n == 0 && cursor >= ce;
             int64_t F = INT64_MAX;

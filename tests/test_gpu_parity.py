@@ -345,3 +345,36 @@ def test_quantize_near_ties_live_reference(ctx, lutname):
         assert kc[i] == len(rt), i
         np.testing.assert_array_equal(kt[i, : kc[i]], rt, err_msg=str(i))
         np.testing.assert_array_equal(kb[i, : kc[i]], rb[:, :D1], err_msg=str(i))
+
+
+@pytest.mark.parametrize("name", ["render_test", "desk", "blob3000", "kd_K6_D6"])
+def test_scene_dataset_stats_on_gpu(ctx, name):
+    """dataset_stats on the resident scene (GPU radix-sort medians + max
+    reduction) equals the host restatement field for field,
+    and both equal the reference's."""
+    g = load(name)
+    lut = S.load_lut(g["lut_path"])
+    ps = g["particles"]
+    for sub in (ps, ps[:-1]):  # even and odd counts
+        ctx.upload(sub, lut)
+        dg = ctx.dataset_stats()
+        dh = S.dataset_stats(sub, lut)
+        dr = ref.dataset_stats(sub, ref.Lut(g["lut_path"]))
+        for k in ("mass_r", "density_r", "h_r", "value_r", "phi_repr", "a_max", "count"):
+            assert getattr(dg, k) == getattr(dh, k), k
+            assert getattr(dg, k) == getattr(dr, k), k
+
+
+def test_scene_dataset_stats_rejects_bad_particles(ctx):
+    lut = S.load_lut(H.lut_path(4, 3, 16))
+    ps = H.random_cloud(H.MT19937_64(3), 50, 1.0, -1.0, 1.0)
+    ps[7, 5] = 0.0  # h = 0
+    ctx.upload(ps, lut)
+    with pytest.raises(S.ConfigError):
+        ctx.dataset_stats()
+
+
+def test_alu_peak_probe():
+    """The bench's ALU-roofline denominators come from a live probe."""
+    pk = S.probe_alu_peaks(0)
+    assert 1e3 < pk["int64_gops"] < 1e6 and 1e3 < pk["fp64_gflops"] < 1e6, pk
