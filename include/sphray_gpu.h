@@ -235,6 +235,28 @@ sphray_status sphray_quantize_hits(sphray_context* ctx, const sphray_particle* p
 sphray_status sphray_compute_dataset_stats(const sphray_particle* particles, size_t n,
                                            const sphray_lut_view* lut, double clustering_factor,
                                            sphray_dataset_stats* out, sphray_error* err);
+/* The reference's `validate` checks (sphray_main.cpp:260-417) on the GPU for
+ * the resident scene and one camera (the reference clamps it to 32 x 32):
+ *   telescoping  -- every touched ray's trailing piece is zero;
+ *   superposition -- every FieldPiece of the render kernel equals the explicit
+ *                   128-bit double sum over the ray's knots (oracle replay);
+ *   dense-L2     -- on the first 64 rays, the L2 distance between the
+ *                   piecewise field and the exact SPH sum (composite Simpson,
+ *                   n = max(64, len / (h_min / 64)) panels) relative to the
+ *                   exact field's L2 norm stays within 4 hypot(E*, Q) on at
+ *                   least 95% of the rays. */
+typedef struct sphray_validate_report {
+    uint64_t telescoping_rays, telescoping_bad;
+    uint64_t superposition_rays, superposition_bad;
+    uint64_t l2_rays, l2_bad;
+    double l2_envelope;
+    double l2_fraction_within;
+    int32_t telescoping_pass, superposition_pass, l2_pass, pass;
+} sphray_validate_report;
+sphray_status sphray_scene_validate(sphray_context* ctx, const sphray_camera* cam,
+                                    const sphray_quanta* qc, const sphray_dataset_stats* ds,
+                                    sphray_validate_report* out, sphray_error* err);
+
 /* dataset_stats (quantize.hpp:129-165) of the scene resident in `ctx`
  * (sphray_scene_upload), on the GPU: radix-sorted medians and a max
  * reduction -- bit-identical to sphray_compute_dataset_stats. */

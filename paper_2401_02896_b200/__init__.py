@@ -102,6 +102,15 @@ class _TfPoint(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("value", "r", "g", "b", "absorption")]
 
 
+class _ValidateReport(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("telescoping_rays", "telescoping_bad",
+                                          "superposition_rays", "superposition_bad",
+                                          "l2_rays", "l2_bad")] + \
+               [("l2_envelope", C.c_double), ("l2_fraction_within", C.c_double)] + \
+               [(n, C.c_int32) for n in ("telescoping_pass", "superposition_pass", "l2_pass",
+                                         "pass_")]
+
+
 class _LutView(C.Structure):
     _fields_ = [("q", C.c_double), ("K", C.c_int32), ("D", C.c_int32), ("N", C.c_int32),
                 ("reserved", C.c_int32), ("records", C.POINTER(C.c_double))]
@@ -186,6 +195,8 @@ def load_library():
                                        P(C.c_int64), P(C.c_int32), P(_Error)]
     L.sphray_compute_dataset_stats.argtypes = [P(_Particle), C.c_size_t, P(_LutView), C.c_double,
                                                P(_DStats), P(_Error)]
+    L.sphray_scene_validate.argtypes = [C.c_void_p, P(_Camera), P(_Quanta), P(_DStats),
+                                        P(_ValidateReport), P(_Error)]
     L.sphray_scene_dataset_stats.argtypes = [C.c_void_p, C.c_double, P(_DStats), P(_Error)]
     L.sphray_choose_quanta.argtypes = [P(_LutView), P(_DStats), C.c_int, C.c_double, C.c_double,
                                        P(_Quanta), P(_Error)]
@@ -564,6 +575,20 @@ class Context:
                                            P(pa, C.c_int64), len(rays), len(pt), C.byref(nr),
                                            C.byref(npc), C.byref(err)), err)
         return dict(rays=rays, piece_off=off, piece_t=pt, piece_a=pa)
+
+    def validate(self, cam: Camera, qc: QuantaConfig, ds: DatasetStats) -> dict:
+        """The reference's `validate` groups (sphray_main.cpp:260-417) for the
+        uploaded scene: telescoping, exact superposition (128-bit replay of
+        every piece), dense-L2 envelope.  Like the reference, callers clamp the
+        camera to 32 x 32 (validate_camera())."""
+        rep, err = _ValidateReport(), _Error()
+        _check(self._L.sphray_scene_validate(self._h, C.byref(cam._c()), C.byref(qc._c()),
+                                             C.byref(ds._c()), C.byref(rep), C.byref(err)), err)
+        out = {k: getattr(rep, k) for k, _ in _ValidateReport._fields_}
+        out["pass"] = bool(out.pop("pass_"))
+        for k in ("telescoping_pass", "superposition_pass", "l2_pass"):
+            out[k] = bool(out[k])
+        return out
 
     def dataset_stats(self, clustering_factor: float = 16.0) -> DatasetStats:
         """dataset_stats (quantize.hpp:129-165) of the uploaded scene, on the GPU."""

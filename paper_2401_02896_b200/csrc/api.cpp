@@ -269,6 +269,15 @@ sphray_status sphray_compute_dataset_stats(const sphray_particle* particles, siz
     });
 }
 
+sphray_status sphray_scene_validate(sphray_context* ctx, const sphray_camera* cam,
+                                    const sphray_quanta* qc, const sphray_dataset_stats* ds,
+                                    sphray_validate_report* out, sphray_error* err) {
+    return guarded(err, [&] {
+        if (!ctx || !cam || !qc || !ds || !out) fail(SPHRAY_ERR_CONFIG, "null argument");
+        ctx->engine->validate(*cam, *qc, *ds, out);
+    });
+}
+
 sphray_status sphray_scene_dataset_stats(sphray_context* ctx, double clustering_factor,
                                          sphray_dataset_stats* out, sphray_error* err) {
     return guarded(err, [&] {

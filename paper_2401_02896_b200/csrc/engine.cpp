@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <numeric>
 #include <string>
 
 namespace sphray_b200 {
@@ -301,6 +302,256 @@ sphray_dataset_stats Engine::scene_dataset_stats(double clustering_factor) {
     for (int e = 0; e < lut_.N; ++e) amp = std::max(amp, entry_amplitude(lut_, e));
     st.a_max = clustering_factor * phi_max * amp;
     return st;
+}
+
+void Engine::validate(const sphray_camera& cam, const sphray_quanta& qc,
+                      const sphray_dataset_stats& ds, sphray_validate_report* rep) {
+    set_device();
+    if (!has_scene_) fail(SPHRAY_ERR_CONFIG, "no scene uploaded");
+    validate_approx(lut_.K, lut_.D);
+    *rep = sphray_validate_report{};
+    const int D = lut_.D, KN = lut_.K + 1, D1 = D + 1;
+    cudaStream_t s = stream_;
+    // ---- hits and pieces of every ray (two dump frames: counts, then data)
+    const sphray_tf_point tf{0.0, 0.0, 0.0, 0.0, 0.0};
+    sphray_render_options opts{};
+    opts.step = 1.0;
+    opts.mode = SPHRAY_MODE_EXACT;
+    sphray_render_stats st{};
+    Dumps d0;
+    d0.hits = d0.pieces = true;
+    render(cam, &tf, 1, qc, ds, opts, nullptr, &st, &d0);
+    Dumps d;
+    d.hits = d.pieces = true;
+    d.cap_hits = d0.n_hits;
+    d.cap_pieces = d0.n_pieces;
+    render(cam, &tf, 1, qc, ds, opts, nullptr, &st, &d);
+    const size_t nh = d.hit_ray.size(), np = d.piece_t.size();
+
+    // ---- pieces: CSR by ray, sorted by t
+    std::vector<size_t> po(np);
+    std::iota(po.begin(), po.end(), size_t{0});
+    std::sort(po.begin(), po.end(), [&](size_t a, size_t b) {
+        return d.piece_ray[a] != d.piece_ray[b] ? d.piece_ray[a] < d.piece_ray[b] : d.piece_t[a] < d.piece_t[b];
+    });
+    std::vector<uint64_t> rays, poff{0};
+    std::vector<int64_t> pt(np), pa(np * D1);
+    std::vector<uint32_t> prow(np);
+    for (size_t i = 0; i < np; ++i) {
+        const size_t o = po[i];
+        if (i == 0 || d.piece_ray[o] != rays.back()) {
+            if (i > 0) poff.push_back(i);
+            rays.push_back(d.piece_ray[o]);
+        }
+        pt[i] = d.piece_t[o];
+        for (int k = 0; k < D1; ++k) pa[i * D1 + k] = d.piece_a[o * D1 + k];
+        prow[i] = static_cast<uint32_t>(rays.size() - 1);
+    }
+    if (np) poff.push_back(np);
+    const size_t nr = rays.size();
+
+    // group 1: telescoping (the trailing piece of every touched ray is zero)
+    rep->telescoping_rays = nr;
+    for (size_t r = 0; r < nr; ++r) {
+        bool zero = true;
+        for (int k = 0; k < D1; ++k) zero &= pa[(poff[r + 1] - 1) * D1 + k] == 0;
+        rep->telescoping_bad += !zero;
+    }
+
+    // ---- knots of every hit: k_quantize_hits on records gathered on the device
+    DevBuf dinv, dpidx, dps, dpw, dpt, dtc, dla, dkt, dkb, dkc;
+    std::vector<int64_t> kt(nh * KN), kb(nh * KN * D1);
+    std::vector<int32_t> kc(nh);
+    if (nh) {
+        std::vector<double> powtau(kMaxDegree, 0.0);
+        for (int k = 1; k <= D; ++k) powtau[k - 1] = std::pow(qc.tau, k);
+        dinv.ensure(n_ * 4);
+        dpidx.ensure(nh * 8);
+        dps.ensure(nh * sizeof(sphray_particle));
+        dpw.ensure(nh * D * 8);
+        dpt.ensure(kMaxDegree * 8);
+        dtc.ensure(nh * 8);
+        dla.ensure(nh * 8);
+        dkt.ensure(kt.size() * 8);
+        dkb.ensure(kb.size() * 8);
+        dkc.ensure(nh * 4);
+        CUDA_OK(cudaMemcpyAsync(dpidx.p, d.hit_pidx.data(), nh * 8, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(dtc.p, d.hit_tchi.data(), nh * 8, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(dla.p, d.hit_lam.data(), nh * 8, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(dpt.p, powtau.data(), kMaxDegree * 8, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemsetAsync(dkt.p, 0, kt.size() * 8, s));
+        CUDA_OK(cudaMemsetAsync(dkb.p, 0, kb.size() * 8, s));
+        launch_hit_records(d_orig_.as<int32_t>(), n_, dinv.as<int32_t>(), dpidx.as<int64_t>(), nh,
+                           d_pxyzh_.as<double4>(), d_mvr_.as<double4>(), d_powh_.as<double>(), D,
+                           dps.as<sphray_particle>(), dpw.as<double>(), s);
+        QuantParams Q{};
+        Q.lut_rows = d_lut_.as<double>();
+        Q.lut_stride = lut_.m + lut_.nj;
+        Q.lut_N = lut_.N;
+        Q.lut_dl = lut_.delta_lambda;
+        Q.q = lut_.q;
+        Q.K = lut_.K;
+        Q.m = lut_.m;
+        Q.tau = qc.tau;
+        Q.sigma = qc.sigma;
+        Q.inv_tau = recip_or_nan(qc.tau);
+        Q.inv_dl = recip_or_nan(lut_.delta_lambda);
+        launch_quantize_hits(Q, D, dps.as<sphray_particle>(), dpw.as<double>(), dpt.as<double>(), nh,
+                             dtc.as<double>(), dla.as<double>(), dkt.as<int64_t>(), dkb.as<int64_t>(),
+                             dkc.as<int32_t>(), s);
+        CUDA_OK(cudaMemcpyAsync(kt.data(), dkt.p, kt.size() * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaMemcpyAsync(kb.data(), dkb.p, kb.size() * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaMemcpyAsync(kc.data(), dkc.p, nh * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        for (size_t i = 0; i < nh; ++i)
+            if (kc[i] < 0)
+                fail(SPHRAY_ERR_OVERFLOW, "validate: quantize overflow", d.hit_pidx[i], d.hit_ray[i]);
+    }
+    // knots: CSR over the same ray rows as the pieces, sorted by t
+    std::vector<std::pair<uint64_t, size_t>> kidx;  // (ray, hit*KN + o)
+    for (size_t i = 0; i < nh; ++i)
+        for (int o = 0; o < kc[i]; ++o) kidx.emplace_back(d.hit_ray[i], i * KN + o);
+    std::sort(kidx.begin(), kidx.end(), [&](const auto& a, const auto& b) {
+        return a.first != b.first ? a.first < b.first : kt[a.second] < kt[b.second];
+    });
+    std::vector<uint64_t> koff(nr + 1, 0);
+    std::vector<int64_t> kts(kidx.size()), kbs(kidx.size() * D1);
+    {
+        size_t r = 0;
+        for (size_t i = 0; i < kidx.size(); ++i) {
+            while (r < nr && rays[r] < kidx[i].first) koff[++r] = i;
+            kts[i] = kt[kidx[i].second];
+            for (int k = 0; k < D1; ++k) kbs[i * D1 + k] = kb[kidx[i].second * D1 + k];
+        }
+        while (r < nr) koff[++r] = kidx.size();
+    }
+
+    // group 2: exact superposition (128-bit explicit replay of every piece)
+    rep->superposition_rays = nr;
+    if (np) {
+        DevBuf a, b, c, e, f, g, h, bad;
+        a.ensure(koff.size() * 8);
+        b.ensure(std::max<size_t>(kts.size(), 1) * 8);
+        c.ensure(std::max<size_t>(kbs.size(), 1) * 8);
+        e.ensure(poff.size() * 8);
+        f.ensure(np * 8);
+        g.ensure(np * D1 * 8);
+        h.ensure(np * 4);
+        bad.ensure(nr * 4);
+        CUDA_OK(cudaMemcpyAsync(a.p, koff.data(), koff.size() * 8, cudaMemcpyHostToDevice, s));
+        if (!kts.empty()) {
+            CUDA_OK(cudaMemcpyAsync(b.p, kts.data(), kts.size() * 8, cudaMemcpyHostToDevice, s));
+            CUDA_OK(cudaMemcpyAsync(c.p, kbs.data(), kbs.size() * 8, cudaMemcpyHostToDevice, s));
+        }
+        CUDA_OK(cudaMemcpyAsync(e.p, poff.data(), poff.size() * 8, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(f.p, pt.data(), np * 8, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(g.p, pa.data(), np * D1 * 8, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(h.p, prow.data(), np * 4, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemsetAsync(bad.p, 0, nr * 4, s));
+        launch_replay(a.as<uint64_t>(), b.as<int64_t>(), c.as<int64_t>(), e.as<uint64_t>(),
+                      f.as<int64_t>(), g.as<int64_t>(), h.as<uint32_t>(), np, D, bad.as<unsigned int>(), s);
+        std::vector<uint32_t> hb(nr);
+        CUDA_OK(cudaMemcpyAsync(hb.data(), bad.p, nr * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        for (size_t r = 0; r < nr; ++r) {
+            // the distinct knot positions are exactly the pieces
+            size_t distinct = 0;
+            for (uint64_t i = koff[r]; i < koff[r + 1]; ++i) distinct += i == koff[r] || kts[i] != kts[i - 1];
+            rep->superposition_bad += hb[r] != 0 || distinct != poff[r + 1] - poff[r];
+        }
+    }
+
+    // group 3: dense-L2 envelope on the first 64 rays (ray-id order)
+    {
+        double acc = 0.0;
+        const double dl = lut_.delta_lambda;
+        for (int e = 0; e < lut_.N; ++e) acc += lut_.lambda[e] * lut_.error[e] * lut_.error[e] * dl;
+        const double estar = std::sqrt(2.0 * M_PI * acc) / kCubicKappa;      // lut.hpp:284-290
+        const double tq = qc.tau / ds.h_r, sq = qc.sigma / ds.phi_repr;       // quantize.hpp:64-73
+        if (!(tq > 0.0)) fail(SPHRAY_ERR_CONFIG, "quantization_error: tau must be positive");
+        if (!(sq >= 0.0)) fail(SPHRAY_ERR_CONFIG, "quantization_error: sigma must be nonnegative");
+        double sacc = kCubicKappaPrime * kCubicKappaPrime * tq * tq;
+        for (int k = 0; k <= D; ++k)
+            sacc += 2.0 * std::pow(lut_.q, 2 * k + 3) / ((2 * k + 1) * (2 * k + 3)) * sq * sq / std::pow(tq, 2 * k);
+        const double qd = std::sqrt(sacc) / (4.0 * kCubicKappa);
+        rep->l2_envelope = 4.0 * std::hypot(estar, qd);
+        // h_min over the particles
+        std::vector<double4> hx(n_);
+        CUDA_OK(cudaMemcpyAsync(hx.data(), d_pxyzh_.p, n_ * sizeof(double4), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        double h_min = n_ ? hx[0].w : 1.0;
+        for (size_t i = 0; i < n_; ++i) h_min = std::min(h_min, hx[i].w);
+        const double h_step = h_min / 64.0;
+        std::vector<uint32_t> ids, rows;
+        std::vector<uint64_t> noff{0};
+        std::vector<double> t0s, dts;
+        std::vector<int> nps;
+        for (size_t r = 0; r < nr && ids.size() < 64; ++r) {
+            const double t0 = static_cast<double>(pt[poff[r]]) * qc.tau;
+            const double t1 = static_cast<double>(pt[poff[r + 1] - 1]) * qc.tau;
+            if (!(t1 > t0)) continue;
+            int n = std::max(64, static_cast<int>((t1 - t0) / h_step));
+            if (n % 2) ++n;  // oracle::simpson (oracle.hpp:38-47)
+            ids.push_back(static_cast<uint32_t>(rays[r]));
+            rows.push_back(static_cast<uint32_t>(r));
+            t0s.push_back(t0);
+            dts.push_back((t1 - t0) / n);
+            nps.push_back(n);
+            noff.push_back(noff.back() + n + 1);
+        }
+        const size_t nn = noff.back();
+        if (!ids.empty()) {
+            DevBuf a, b, c, e, f, g, h, ap, ex;
+            a.ensure(ids.size() * 4);
+            b.ensure(noff.size() * 8);
+            c.ensure(ids.size() * 8);
+            e.ensure(ids.size() * 8);
+            f.ensure(poff.size() * 8);
+            g.ensure(rows.size() * 4);
+            h.ensure(np * 8 + np * D1 * 8);
+            ap.ensure(nn * 8);
+            ex.ensure(nn * 8);
+            CUDA_OK(cudaMemcpyAsync(a.p, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, s));
+            CUDA_OK(cudaMemcpyAsync(b.p, noff.data(), noff.size() * 8, cudaMemcpyHostToDevice, s));
+            CUDA_OK(cudaMemcpyAsync(c.p, t0s.data(), t0s.size() * 8, cudaMemcpyHostToDevice, s));
+            CUDA_OK(cudaMemcpyAsync(e.p, dts.data(), dts.size() * 8, cudaMemcpyHostToDevice, s));
+            CUDA_OK(cudaMemcpyAsync(f.p, poff.data(), poff.size() * 8, cudaMemcpyHostToDevice, s));
+            CUDA_OK(cudaMemcpyAsync(g.p, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, s));
+            int64_t* dpt_ = h.as<int64_t>();
+            CUDA_OK(cudaMemcpyAsync(dpt_, pt.data(), np * 8, cudaMemcpyHostToDevice, s));
+            CUDA_OK(cudaMemcpyAsync(dpt_ + np, pa.data(), np * D1 * 8, cudaMemcpyHostToDevice, s));
+            const CamConst C = make_camera(cam);
+            launch_l2_nodes(C, a.as<uint32_t>(), static_cast<int>(ids.size()), b.as<uint64_t>(),
+                            c.as<double>(), e.as<double>(), f.as<uint64_t>(), g.as<uint32_t>(), dpt_,
+                            dpt_ + np, D, qc.tau, qc.sigma, d_pxyzh_.as<double4>(), d_mvr_.as<double4>(),
+                            n_, ap.as<double>(), ex.as<double>(), s);
+            std::vector<double> hap(nn), hex(nn);
+            CUDA_OK(cudaMemcpyAsync(hap.data(), ap.p, nn * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_OK(cudaMemcpyAsync(hex.data(), ex.p, nn * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_OK(cudaStreamSynchronize(s));
+            for (size_t r = 0; r < ids.size(); ++r) {
+                const int n = nps[r];
+                const double hh = dts[r];
+                double num = 0.0, den = 0.0;
+                for (int i = 0; i <= n; ++i) {
+                    const double w = (i == 0 || i == n) ? 1.0 : (i % 2 ? 4.0 : 2.0);
+                    const double dv = hap[noff[r] + i] - hex[noff[r] + i];
+                    num += w * dv * dv;
+                    den += w * hex[noff[r] + i] * hex[noff[r] + i];
+                }
+                num = std::sqrt(std::max(num * hh / 3.0, 0.0));
+                den = std::sqrt(std::max(den * hh / 3.0, 0.0));
+                ++rep->l2_rays;
+                if (den > 0.0 && num / den > rep->l2_envelope) ++rep->l2_bad;
+            }
+        }
+        rep->l2_fraction_within =
+            rep->l2_rays ? static_cast<double>(rep->l2_rays - rep->l2_bad) / rep->l2_rays : 1.0;
+    }
+    rep->telescoping_pass = rep->telescoping_bad == 0;
+    rep->superposition_pass = rep->superposition_bad == 0;
+    rep->l2_pass = rep->l2_fraction_within >= 0.95;
+    rep->pass = rep->telescoping_pass && rep->superposition_pass && rep->l2_pass;
 }
 
 void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t ntf,

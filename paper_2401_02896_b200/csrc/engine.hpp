@@ -57,6 +57,9 @@ class Engine {
     void upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_view& lut);
     // dataset_stats (quantize.hpp:129-165) of the uploaded scene, computed on the GPU
     sphray_dataset_stats scene_dataset_stats(double clustering_factor);
+    // the reference's validate groups for the resident scene (validate.cu)
+    void validate(const sphray_camera& cam, const sphray_quanta& qc, const sphray_dataset_stats& ds,
+                  sphray_validate_report* out);
     // Renders the resident scene.  rgb_host may be null (image stays on device).
     void render(const sphray_camera& cam, const sphray_tf_point* tf, size_t ntf,
                 const sphray_quanta& qc, const sphray_dataset_stats& ds,

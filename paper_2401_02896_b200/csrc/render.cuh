@@ -147,6 +147,20 @@ int max_blocks_per_sm(int D, int m, int warps, size_t smem);
 // dataset_stats (quantize.hpp:129-165) of the resident scene: medians of
 // mass, density, h, value (med[0..3]), phi_max, and whether some particle has
 // h <= 0 or density <= 0.
+// validate.cu
+void launch_hit_records(const int32_t* orig, size_t n, int32_t* inv, const int64_t* pidx, size_t nh,
+                        const double4* pxyzh, const double4* mvr, const double* powh, int D,
+                        sphray_particle* out, double* powh_out, cudaStream_t s);
+void launch_replay(const uint64_t* knot_off, const int64_t* knot_t, const int64_t* knot_b,
+                   const uint64_t* piece_off, const int64_t* piece_t, const int64_t* piece_a,
+                   const uint32_t* piece_ray, size_t npieces, int D, unsigned int* ray_bad,
+                   cudaStream_t s);
+void launch_l2_nodes(const CamConst& cam, const uint32_t* ray_ids, int nrays, const uint64_t* node_off,
+                     const double* t0, const double* dtn, const uint64_t* piece_off,
+                     const uint32_t* ray_piece_row, const int64_t* piece_t, const int64_t* piece_a,
+                     int D, double tau, double sigma, const double4* pxyzh, const double4* mvr,
+                     size_t n, double* approx, double* exact, cudaStream_t s);
+
 void device_dataset_stats(const double4* pxyzh, const double4* mvr, size_t n, cudaStream_t s,
                           double med[4], double* phi_max, bool* bad);
 void launch_render(const FrameParams& P, int D, int m, int blocks, int warps, cudaStream_t s);
