@@ -257,6 +257,25 @@ sphray_status sphray_scene_validate(sphray_context* ctx, const sphray_camera* ca
                                     const sphray_quanta* qc, const sphray_dataset_stats* ds,
                                     sphray_validate_report* out, sphray_error* err);
 
+/* -------------------------------------------------------------------------
+ * File formats (io.hpp:62-216): SPRT binary / CSV particles (format sniffed
+ * by magic), transfer-function CSV, binary PPM.  Loaders allocate with
+ * malloc; release with sphray_free.  Errors: SPHRAY_ERR_IO (ConfigError for an
+ * invalid transfer function, as the reference).
+ * ---------------------------------------------------------------------- */
+sphray_status sphray_particles_load(const char* path, sphray_particle** out, size_t* n,
+                                    sphray_error* err);
+sphray_status sphray_particles_save(const char* path, const sphray_particle* particles, size_t n,
+                                    int binary, sphray_error* err);
+sphray_status sphray_tf_load(const char* path, sphray_tf_point** out, size_t* n, sphray_error* err);
+sphray_status sphray_ppm_save(const char* path, const double* rgb, int width, int height,
+                              sphray_error* err);
+void sphray_free(void* p);
+/* Loads a particle file and uploads it as the scene of `ctx`
+ * (sphray_scene_upload semantics). */
+sphray_status sphray_scene_upload_file(sphray_context* ctx, const char* path,
+                                       const sphray_lut_view* lut, sphray_error* err);
+
 /* dataset_stats (quantize.hpp:129-165) of the scene resident in `ctx`
  * (sphray_scene_upload), on the GPU: radix-sorted medians and a max
  * reduction -- bit-identical to sphray_compute_dataset_stats. */

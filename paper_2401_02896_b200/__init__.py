@@ -195,6 +195,12 @@ def load_library():
                                        P(C.c_int64), P(C.c_int32), P(_Error)]
     L.sphray_compute_dataset_stats.argtypes = [P(_Particle), C.c_size_t, P(_LutView), C.c_double,
                                                P(_DStats), P(_Error)]
+    L.sphray_particles_load.argtypes = [C.c_char_p, P(P(_Particle)), P(C.c_size_t), P(_Error)]
+    L.sphray_particles_save.argtypes = [C.c_char_p, P(_Particle), C.c_size_t, C.c_int, P(_Error)]
+    L.sphray_tf_load.argtypes = [C.c_char_p, P(P(_TfPoint)), P(C.c_size_t), P(_Error)]
+    L.sphray_ppm_save.argtypes = [C.c_char_p, P(C.c_double), C.c_int, C.c_int, P(_Error)]
+    L.sphray_free.argtypes = [C.c_void_p]
+    L.sphray_scene_upload_file.argtypes = [C.c_void_p, C.c_char_p, P(_LutView), P(_Error)]
     L.sphray_scene_validate.argtypes = [C.c_void_p, P(_Camera), P(_Quanta), P(_DStats),
                                         P(_ValidateReport), P(_Error)]
     L.sphray_scene_dataset_stats.argtypes = [C.c_void_p, C.c_double, P(_DStats), P(_Error)]
@@ -433,6 +439,48 @@ def choose_quanta(lut: Lut, stats: DatasetStats, width: int = 64,
     _check(L.sphray_choose_quanta(C.byref(lut.view), C.byref(ds), int(width), kappa, kappa_prime,
                                   C.byref(out), C.byref(err)), err)
     return QuantaConfig(out.tau, out.sigma, out.int_width)
+
+
+def load_particles(path: str) -> np.ndarray:
+    """load_particles (io.hpp:141-151): SPRT binary or CSV -> (n, 7) float64
+    rows x, y, z, mass, density, h, value."""
+    L = load_library()
+    ptr, n, err = C.POINTER(_Particle)(), C.c_size_t(), _Error()
+    _check(L.sphray_particles_load(os.fsencode(path), C.byref(ptr), C.byref(n), C.byref(err)), err)
+    try:
+        out = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_double)), shape=(n.value * 7,)).copy()
+    finally:
+        L.sphray_free(ptr)
+    return out.reshape(n.value, 7)
+
+
+def save_particles(particles, path: str, binary: bool = False) -> None:
+    """save_particles (io.hpp:153-161)."""
+    L = load_library()
+    a = _particles(particles)
+    err = _Error()
+    _check(L.sphray_particles_save(os.fsencode(path), _pp(a), len(a), int(binary), C.byref(err)), err)
+
+
+def load_transfer_function(path: str) -> "TransferFunction":
+    """load_transfer_function (io.hpp:158-190): sorted, validated."""
+    L = load_library()
+    ptr, n, err = C.POINTER(_TfPoint)(), C.c_size_t(), _Error()
+    _check(L.sphray_tf_load(os.fsencode(path), C.byref(ptr), C.byref(n), C.byref(err)), err)
+    try:
+        arr = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_double)), shape=(n.value * 5,)).copy()
+    finally:
+        L.sphray_free(ptr)
+    return TransferFunction.from_array(arr.reshape(n.value, 5))
+
+
+def save_ppm(rgb, path: str) -> None:
+    """save_ppm (io.hpp:193-210): (H, W, 3) linear RGB clamped to [0, 1], 8 bits."""
+    L = load_library()
+    a = np.ascontiguousarray(rgb, dtype=np.float64)
+    err = _Error()
+    _check(L.sphray_ppm_save(os.fsencode(path), a.ctypes.data_as(C.POINTER(C.c_double)),
+                             a.shape[1], a.shape[0], C.byref(err)), err)
 
 
 def probe_alu_peaks(device: int = 0) -> dict:

@@ -4,6 +4,7 @@
 #include <cstring>
 #include <memory>
 #include <numeric>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -275,6 +276,62 @@ sphray_status sphray_scene_validate(sphray_context* ctx, const sphray_camera* ca
     return guarded(err, [&] {
         if (!ctx || !cam || !qc || !ds || !out) fail(SPHRAY_ERR_CONFIG, "null argument");
         ctx->engine->validate(*cam, *qc, *ds, out);
+    });
+}
+
+sphray_status sphray_particles_load(const char* path, sphray_particle** out, size_t* n,
+                                    sphray_error* err) {
+    return guarded(err, [&] {
+        if (!path || !out || !n) fail(SPHRAY_ERR_CONFIG, "null argument");
+        *out = nullptr;
+        *n = 0;
+        const auto ps = load_particles(path);
+        auto* buf = static_cast<sphray_particle*>(std::malloc(std::max<size_t>(ps.size(), 1) * sizeof(sphray_particle)));
+        if (!buf) fail(SPHRAY_ERR_IO, "out of host memory");
+        std::memcpy(buf, ps.data(), ps.size() * sizeof(sphray_particle));
+        *out = buf;
+        *n = ps.size();
+    });
+}
+
+sphray_status sphray_particles_save(const char* path, const sphray_particle* particles, size_t n,
+                                    int binary, sphray_error* err) {
+    return guarded(err, [&] {
+        if (!path || (n && !particles)) fail(SPHRAY_ERR_CONFIG, "null argument");
+        save_particles(particles, n, path, binary != 0);
+    });
+}
+
+sphray_status sphray_tf_load(const char* path, sphray_tf_point** out, size_t* n, sphray_error* err) {
+    return guarded(err, [&] {
+        if (!path || !out || !n) fail(SPHRAY_ERR_CONFIG, "null argument");
+        *out = nullptr;
+        *n = 0;
+        const auto tf = load_transfer_function(path);
+        auto* buf = static_cast<sphray_tf_point*>(std::malloc(std::max<size_t>(tf.size(), 1) * sizeof(sphray_tf_point)));
+        if (!buf) fail(SPHRAY_ERR_IO, "out of host memory");
+        std::memcpy(buf, tf.data(), tf.size() * sizeof(sphray_tf_point));
+        *out = buf;
+        *n = tf.size();
+    });
+}
+
+sphray_status sphray_ppm_save(const char* path, const double* rgb, int width, int height,
+                              sphray_error* err) {
+    return guarded(err, [&] {
+        if (!path || (width > 0 && height > 0 && !rgb)) fail(SPHRAY_ERR_CONFIG, "null argument");
+        save_ppm(rgb, width, height, path);
+    });
+}
+
+void sphray_free(void* p) { std::free(p); }
+
+sphray_status sphray_scene_upload_file(sphray_context* ctx, const char* path,
+                                       const sphray_lut_view* lut, sphray_error* err) {
+    return guarded(err, [&] {
+        if (!ctx || !path || !lut) fail(SPHRAY_ERR_CONFIG, "null argument");
+        const auto ps = load_particles(path);
+        ctx->engine->upload_scene(ps.data(), ps.size(), *lut);
     });
 }
 

@@ -230,17 +230,6 @@ void Engine::upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_
 }
 
 namespace {
-// TransferFunction::validate (raycast.hpp:316-324)
-void validate_tf(const sphray_tf_point* tf, size_t ntf) {
-    if (ntf == 0 || !tf) fail(SPHRAY_ERR_CONFIG, "transfer function: no control points");
-    for (size_t i = 0; i < ntf; ++i) {
-        if (tf[i].absorption < 0.0)
-            fail(SPHRAY_ERR_CONFIG, "transfer function: absorption must be nonnegative");
-        if (i > 0 && !(tf[i].value > tf[i - 1].value))
-            fail(SPHRAY_ERR_CONFIG, "transfer function: values must be strictly increasing");
-    }
-}
-
 // TransferFunction::sample(0).absorption (raycast.hpp:326-337)
 double tf_absorption_at_zero(const sphray_tf_point* p, size_t n) {
     const double v = 0.0;

@@ -286,6 +286,17 @@ double median(std::vector<double> v) {  // quantize.hpp:118-122
 }
 }  // namespace
 
+// TransferFunction::validate (raycast.hpp:316-324)
+void validate_tf(const sphray_tf_point* tf, size_t ntf) {
+    if (ntf == 0 || !tf) fail(SPHRAY_ERR_CONFIG, "transfer function: no control points");
+    for (size_t i = 0; i < ntf; ++i) {
+        if (tf[i].absorption < 0.0)
+            fail(SPHRAY_ERR_CONFIG, "transfer function: absorption must be nonnegative");
+        if (i > 0 && !(tf[i].value > tf[i - 1].value))
+            fail(SPHRAY_ERR_CONFIG, "transfer function: values must be strictly increasing");
+    }
+}
+
 // dataset_stats, quantize.hpp:129-165.
 sphray_dataset_stats dataset_stats(const sphray_particle* ps, size_t n, const LutHost& L,
                                    double clustering_factor) {

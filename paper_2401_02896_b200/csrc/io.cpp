@@ -1,0 +1,179 @@
+// io.cpp -- the reference's particle / transfer-function readers and PPM
+// writer (io.hpp:62-216), restated so a caller of the C ABI needs nothing
+// from the reference to feed the renderer.  Same accepted
+// syntax (std::stod numbers, comma cells trimmed of white space, SPRT binary
+// sniffed by magic), same validation and the same exception classes.
+#include <algorithm>
+#include <cctype>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "host.hpp"
+
+namespace sphray_b200 {
+namespace {
+
+std::string trim(std::string s) {  // io.hpp:38-43
+    const auto notspace = [](unsigned char c) { return !std::isspace(c); };
+    s.erase(s.begin(), std::find_if(s.begin(), s.end(), notspace));
+    s.erase(std::find_if(s.rbegin(), s.rend(), notspace).base(), s.end());
+    return s;
+}
+
+std::vector<std::string> split_row(const std::string& line) {  // io.hpp:45-51
+    std::vector<std::string> out;
+    std::stringstream ss(line);
+    std::string cell;
+    while (std::getline(ss, cell, ',')) out.push_back(trim(cell));
+    return out;
+}
+
+double number(const std::string& s, const std::string& where) {  // io.hpp:53-61
+    try {
+        std::size_t pos = 0;
+        const double v = std::stod(s, &pos);
+        if (pos != s.size()) throw std::invalid_argument(s);
+        return v;
+    } catch (const std::exception&) {
+        fail(SPHRAY_ERR_IO, where + ": not a number: '" + s + "'");
+    }
+}
+
+void check_particle(const sphray_particle& p, const std::string& where) {  // io.hpp:63-68
+    if (!(p.h > 0.0)) fail(SPHRAY_ERR_IO, where + ": smoothing radius must be positive");
+    if (!(p.density > 0.0)) fail(SPHRAY_ERR_IO, where + ": density must be positive");
+    for (double v : {p.x, p.y, p.z, p.mass, p.value})
+        if (!std::isfinite(v)) fail(SPHRAY_ERR_IO, where + ": attribute not finite");
+}
+
+uint64_t le64(const unsigned char* b) {
+    uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= static_cast<uint64_t>(b[i]) << (8 * i);
+    return v;
+}
+
+constexpr const char* kCsvHeader = "x,y,z,mass,density,h,value";  // io.hpp:72
+
+}  // namespace
+
+std::vector<sphray_particle> load_particles(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) fail(SPHRAY_ERR_IO, "cannot open particle file " + path);
+    char magic[4] = {};
+    f.read(magic, 4);
+    f.clear();
+    f.seekg(0);
+    std::vector<sphray_particle> out;
+    if (std::memcmp(magic, "SPRT", 4) == 0) {  // read_particles_binary, io.hpp:118-138
+        std::vector<unsigned char> buf((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+        if (buf.size() < 12) fail(SPHRAY_ERR_IO, "truncated file");
+        const uint64_t n = le64(buf.data() + 4);
+        if ((buf.size() - 12) / 56 < n) fail(SPHRAY_ERR_IO, "lut: truncated file");
+        out.resize(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            double v[7];
+            for (int k = 0; k < 7; ++k) {
+                const uint64_t bits = le64(buf.data() + 12 + i * 56 + k * 8);
+                std::memcpy(&v[k], &bits, 8);
+            }
+            sphray_particle& p = out[i];
+            p = sphray_particle{v[0], v[1], v[2], v[3], v[4], v[5], v[6]};
+            check_particle(p, path + ": record " + std::to_string(i));
+        }
+        return out;
+    }
+    // read_particles_csv, io.hpp:74-99
+    std::string line;
+    if (!std::getline(f, line)) fail(SPHRAY_ERR_IO, path + ": empty file");
+    if (trim(line) != kCsvHeader)
+        fail(SPHRAY_ERR_IO, path + ": first line must be '" + std::string(kCsvHeader) + "'");
+    std::size_t lineno = 1;
+    while (std::getline(f, line)) {
+        ++lineno;
+        if (trim(line).empty()) continue;
+        const auto c = split_row(line);
+        const std::string where = path + ":" + std::to_string(lineno);
+        if (c.size() != 7) fail(SPHRAY_ERR_IO, where + ": expected 7 comma-separated values");
+        sphray_particle p{number(c[0], where), number(c[1], where), number(c[2], where),
+                          number(c[3], where), number(c[4], where), number(c[5], where),
+                          number(c[6], where)};
+        check_particle(p, where);
+        out.push_back(p);
+    }
+    return out;
+}
+
+void save_particles(const sphray_particle* ps, size_t n, const std::string& path, bool binary) {
+    std::ofstream f(path, std::ios::binary);
+    if (!f) fail(SPHRAY_ERR_IO, "cannot open " + path + " for writing");
+    if (binary) {  // write_particles_binary, io.hpp:109-116
+        f.write("SPRT", 4);
+        unsigned char b[8];
+        for (int i = 0; i < 8; ++i) b[i] = static_cast<unsigned char>(static_cast<uint64_t>(n) >> (8 * i));
+        f.write(reinterpret_cast<const char*>(b), 8);
+        for (size_t k = 0; k < n; ++k) {
+            const double v[7] = {ps[k].x, ps[k].y, ps[k].z, ps[k].mass, ps[k].density, ps[k].h, ps[k].value};
+            for (double d : v) {
+                uint64_t bits;
+                std::memcpy(&bits, &d, 8);
+                for (int i = 0; i < 8; ++i) b[i] = static_cast<unsigned char>(bits >> (8 * i));
+                f.write(reinterpret_cast<const char*>(b), 8);
+            }
+        }
+        if (!f) fail(SPHRAY_ERR_IO, "particle binary: write failure");
+    } else {  // write_particles_csv, io.hpp:101-107
+        f << kCsvHeader << "\n";
+        f.precision(17);
+        for (size_t k = 0; k < n; ++k) {
+            const auto& p = ps[k];
+            f << p.x << ',' << p.y << ',' << p.z << ',' << p.mass << ',' << p.density << ','
+              << p.h << ',' << p.value << "\n";
+        }
+        if (!f) fail(SPHRAY_ERR_IO, "particle csv: write failure");
+    }
+}
+
+std::vector<sphray_tf_point> load_transfer_function(const std::string& path) {
+    std::ifstream f(path);
+    if (!f) fail(SPHRAY_ERR_IO, "cannot open transfer function " + path);
+    std::vector<sphray_tf_point> pts;  // read_transfer_function_csv, io.hpp:158-184
+    std::string line;
+    std::size_t lineno = 0;
+    while (std::getline(f, line)) {
+        ++lineno;
+        const std::string t = trim(line);
+        if (t.empty()) continue;
+        if (lineno == 1 && !std::isdigit(static_cast<unsigned char>(t[0])) && t[0] != '-' &&
+            t[0] != '+' && t[0] != '.')
+            continue;  // header
+        const auto c = split_row(t);
+        const std::string where = path + ":" + std::to_string(lineno);
+        if (c.size() != 5) fail(SPHRAY_ERR_IO, where + ": expected value,r,g,b,absorption");
+        pts.push_back(sphray_tf_point{number(c[0], where), number(c[1], where), number(c[2], where),
+                                      number(c[3], where), number(c[4], where)});
+    }
+    std::sort(pts.begin(), pts.end(),
+              [](const sphray_tf_point& a, const sphray_tf_point& b) { return a.value < b.value; });
+    validate_tf(pts.data(), pts.size());  // TransferFunction::validate, raycast.hpp:316-324
+    return pts;
+}
+
+void save_ppm(const double* rgb, int W, int H, const std::string& path) {  // io.hpp:193-210
+    if (W < 0 || H < 0) fail(SPHRAY_ERR_CONFIG, "ppm: negative size");
+    std::ofstream f(path, std::ios::binary);
+    if (!f) fail(SPHRAY_ERR_IO, "cannot open " + path + " for writing");
+    f << "P6\n" << W << " " << H << "\n255\n";
+    const size_t n = static_cast<size_t>(W) * H * 3;
+    std::string bytes(n, '\0');
+    for (size_t i = 0; i < n; ++i)
+        bytes[i] = static_cast<char>(static_cast<int>(std::lround(255.0 * std::clamp(rgb[i], 0.0, 1.0))));
+    f.write(bytes.data(), static_cast<std::streamsize>(n));
+    if (!f) fail(SPHRAY_ERR_IO, "ppm: write failure");
+}
+
+}  // namespace sphray_b200
