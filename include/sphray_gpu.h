@@ -270,6 +270,9 @@ sphray_status sphray_particles_save(const char* path, const sphray_particle* par
 sphray_status sphray_tf_load(const char* path, sphray_tf_point** out, size_t* n, sphray_error* err);
 sphray_status sphray_ppm_save(const char* path, const double* rgb, int width, int height,
                               sphray_error* err);
+/* load_camera (io.hpp:263-304): camera JSON with the reference's defaults,
+ * validated like Camera::validate (ConfigError) */
+sphray_status sphray_camera_load(const char* path, sphray_camera* out, sphray_error* err);
 void sphray_free(void* p);
 /* Loads a particle file and uploads it as the scene of `ctx`
  * (sphray_scene_upload semantics). */

@@ -200,6 +200,7 @@ def load_library():
     L.sphray_tf_load.argtypes = [C.c_char_p, P(P(_TfPoint)), P(C.c_size_t), P(_Error)]
     L.sphray_ppm_save.argtypes = [C.c_char_p, P(C.c_double), C.c_int, C.c_int, P(_Error)]
     L.sphray_free.argtypes = [C.c_void_p]
+    L.sphray_camera_load.argtypes = [C.c_char_p, P(_Camera), P(_Error)]
     L.sphray_scene_upload_file.argtypes = [C.c_void_p, C.c_char_p, P(_LutView), P(_Error)]
     L.sphray_scene_validate.argtypes = [C.c_void_p, P(_Camera), P(_Quanta), P(_DStats),
                                         P(_ValidateReport), P(_Error)]
@@ -472,6 +473,17 @@ def load_transfer_function(path: str) -> "TransferFunction":
     finally:
         L.sphray_free(ptr)
     return TransferFunction.from_array(arr.reshape(n.value, 5))
+
+
+def load_camera(path: str) -> "Camera":
+    """load_camera (io.hpp:294-304)."""
+    L = load_library()
+    c, err = _Camera(), _Error()
+    _check(L.sphray_camera_load(os.fsencode(path), C.byref(c), C.byref(err)), err)
+    return Camera(mode="pinhole" if c.mode == 1 else "orthographic", position=tuple(c.position),
+                  look_at=tuple(c.look_at), up=tuple(c.up), width=c.width, height=c.height,
+                  fov_deg=c.fov_deg, ortho_height=c.ortho_height, near=c.near_plane,
+                  far=c.far_plane)
 
 
 def save_ppm(rgb, path: str) -> None:

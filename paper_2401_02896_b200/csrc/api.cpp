@@ -324,6 +324,13 @@ sphray_status sphray_ppm_save(const char* path, const double* rgb, int width, in
     });
 }
 
+sphray_status sphray_camera_load(const char* path, sphray_camera* out, sphray_error* err) {
+    return guarded(err, [&] {
+        if (!path || !out) fail(SPHRAY_ERR_CONFIG, "null argument");
+        *out = load_camera(path);
+    });
+}
+
 void sphray_free(void* p) { std::free(p); }
 
 sphray_status sphray_scene_upload_file(sphray_context* ctx, const char* path,

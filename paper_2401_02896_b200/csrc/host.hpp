@@ -79,6 +79,7 @@ std::vector<sphray_particle> load_particles(const std::string& path);
 void save_particles(const sphray_particle* ps, size_t n, const std::string& path, bool binary);
 std::vector<sphray_tf_point> load_transfer_function(const std::string& path);
 void save_ppm(const double* rgb, int W, int H, const std::string& path);
+sphray_camera load_camera(const std::string& path);
 
 // probe.cu: measured issue peaks (int64 mul/add ops/s, fp64 flops/s) of this GPU
 void probe_alu_peaks(int device, double* int64_gops, double* fp64_gflops);

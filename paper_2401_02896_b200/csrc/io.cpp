@@ -15,6 +15,10 @@
 
 #include "host.hpp"
 
+#if SPHRAY_HAVE_JSON
+#include "json.hpp"
+#endif
+
 namespace sphray_b200 {
 namespace {
 
@@ -174,6 +178,58 @@ void save_ppm(const double* rgb, int W, int H, const std::string& path) {  // io
         bytes[i] = static_cast<char>(static_cast<int>(std::lround(255.0 * std::clamp(rgb[i], 0.0, 1.0))));
     f.write(bytes.data(), static_cast<std::streamsize>(n));
     if (!f) fail(SPHRAY_ERR_IO, "ppm: write failure");
+}
+
+// load_camera / camera_from_json (io.hpp:263-304): defaults of sphray::Camera
+// (raycast.hpp:45-57), then Camera::validate.
+sphray_camera load_camera(const std::string& path) {
+#if SPHRAY_HAVE_JSON
+    std::ifstream f(path);
+    if (!f) fail(SPHRAY_ERR_IO, "cannot open camera file " + path);
+    nlohmann::json j;
+    try {
+        f >> j;
+    } catch (const nlohmann::json::exception& e) {
+        fail(SPHRAY_ERR_IO, path + ": " + e.what());
+    }
+    sphray_camera c{};
+    c.mode = 0;
+    c.look_at[2] = -1.0;
+    c.up[1] = 1.0;
+    c.width = c.height = 64;
+    c.fov_deg = 60.0;
+    c.ortho_height = 2.0;
+    c.near_plane = 0.0;
+    c.far_plane = 1e30;
+    auto vec3 = [](const nlohmann::json& v, double (&out)[3]) {
+        if (!v.is_array() || v.size() != 3) fail(SPHRAY_ERR_IO, "camera json: expected [x, y, z]");
+        for (int i = 0; i < 3; ++i) out[i] = v.at(i).get<double>();
+    };
+    try {
+        const std::string mode = j.value("mode", std::string("orthographic"));
+        if (mode == "orthographic")
+            c.mode = 0;
+        else if (mode == "pinhole")
+            c.mode = 1;
+        else
+            fail(SPHRAY_ERR_IO, "camera json: mode must be 'orthographic' or 'pinhole'");
+        if (j.contains("position")) vec3(j.at("position"), c.position);
+        if (j.contains("look_at")) vec3(j.at("look_at"), c.look_at);
+        if (j.contains("up")) vec3(j.at("up"), c.up);
+        c.width = j.value("width", c.width);
+        c.height = j.value("height", c.height);
+        c.fov_deg = j.value("fov_deg", c.fov_deg);
+        c.ortho_height = j.value("ortho_height", c.ortho_height);
+        c.near_plane = j.value("near", c.near_plane);
+        c.far_plane = j.value("far", c.far_plane);
+    } catch (const nlohmann::json::exception& e) {
+        fail(SPHRAY_ERR_IO, std::string("camera json: ") + e.what());
+    }
+    (void)make_camera(c);  // Camera::validate (raycast.hpp:59-68)
+    return c;
+#else
+    fail(SPHRAY_ERR_IO, "camera json: library built without nlohmann/json (" + path + ")");
+#endif
 }
 
 }  // namespace sphray_b200

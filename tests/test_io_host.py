@@ -142,3 +142,31 @@ def test_bundled_desk_files_if_present():
                 continue
             a = S.load_particles(p)
             assert (a.view(np.uint64) == b.view(np.uint64)).all(), f
+
+
+CAM_CASES = {
+    "bundled_like": '{"mode": "pinhole", "position": [0.0, 0.55, 3.4], "look_at": [0,0,0], '
+                    '"up": [0,1,0], "width": 256, "height": 192, "fov_deg": 42.0, "near": 0.0, "far": 100.0}',
+    "defaults": "{}",
+    "ortho": '{"mode": "orthographic", "position": [0,0,8], "look_at": [0,0,0], "ortho_height": 6}',
+    "bad_mode": '{"mode": "fisheye"}',
+    "bad_vec": '{"position": [0, 1]}',
+    "bad_json": '{"mode": ',
+    "zero_width": '{"width": 0}',
+    "degenerate_up": '{"position": [0,0,0], "look_at": [0,1,0], "up": [0,1,0]}',
+    "bad_fov": '{"mode": "pinhole", "fov_deg": 180}',
+    "string_width": '{"width": "wide"}',
+}
+
+
+@pytest.mark.parametrize("case", sorted(CAM_CASES))
+def test_camera_json_matches_reference(tmp_path, case):
+    path = str(tmp_path / "cam.json")
+    open(path, "w").write(CAM_CASES[case])
+    a, va = outcome_ours(S.load_camera, path)
+    b, vb = outcome_ref(ref.load_camera, path)
+    assert a == b, (case, a, b)
+    if a == "ok":
+        for k in ("mode", "position", "look_at", "up", "width", "height", "fov_deg",
+                  "ortho_height", "near", "far"):
+            assert getattr(va, k) == getattr(vb, k) or tuple(getattr(va, k)) == tuple(getattr(vb, k)), k
