@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <thread>
 #include <numeric>
 #include <string>
 
@@ -126,6 +127,8 @@ Engine::Engine(int device) : device_(device) {
         fail(SPHRAY_ERR_CUDA, std::string("device ") + prop.name + " is not sm_100 (B200) class");
     sm_count_ = prop.multiProcessorCount;
     CUDA_OK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&ev_aux_, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreate(&ev0_));
     CUDA_OK(cudaEventCreate(&ev1_));
     CUDA_OK(cudaEventCreate(&evb_));
@@ -136,9 +139,10 @@ Engine::Engine(int device) : device_(device) {
 Engine::~Engine() {
     cudaSetDevice(device_);
     if (comm_ && nccl().ok) nccl().CommDestroy(static_cast<ncclComm_t>(comm_));
-    for (cudaEvent_t e : {ev0_, ev1_, evb_, evr0_, evr1_})
+    for (cudaEvent_t e : {ev0_, ev1_, evb_, evr0_, evr1_, ev_aux_})
         if (e) cudaEventDestroy(e);
     if (stream_) cudaStreamDestroy(stream_);
+    if (aux_) cudaStreamDestroy(aux_);
 }
 
 void Engine::set_device() const { CUDA_OK(cudaSetDevice(device_)); }
@@ -186,29 +190,30 @@ void Engine::upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_
         CUDA_OK(cudaStreamSynchronize(stream_));
         return;
     }
-    // pow(h, d+3) with glibc (quantize.hpp:222): the one libm call per particle
+    // The raw particles go up on the aux stream from a helper thread (a
+    // pageable copy holds its calling thread) while this thread computes
+    // pow(h, d+3) with glibc (quantize.hpp:222, the one libm call per
+    // particle) and the bounding box for the Morton codes.
+    d_raw_.ensure(n * sizeof(sphray_particle));
+    d_powh_raw_.ensure(n * D * sizeof(double));
+    cudaError_t copy_rc = cudaSuccess;
+    std::thread copier([&] {
+        copy_rc = cudaSetDevice(device_);
+        if (copy_rc == cudaSuccess)
+            copy_rc = cudaMemcpyAsync(d_raw_.p, ps, n * sizeof(sphray_particle), cudaMemcpyHostToDevice, aux_);
+        if (copy_rc == cudaSuccess) copy_rc = cudaStreamSynchronize(aux_);
+    });
     h_powh_.resize(n * D);
-    particle_powers(ps, n, D, h_powh_.data());
-    double lo[3] = {ps[0].x, ps[0].y, ps[0].z}, hi[3] = {ps[0].x, ps[0].y, ps[0].z};
-    for (size_t i = 1; i < n; ++i) {
-        lo[0] = std::min(lo[0], ps[i].x);
-        lo[1] = std::min(lo[1], ps[i].y);
-        lo[2] = std::min(lo[2], ps[i].z);
-        hi[0] = std::max(hi[0], ps[i].x);
-        hi[1] = std::max(hi[1], ps[i].y);
-        hi[2] = std::max(hi[2], ps[i].z);
-    }
+    double lo[3], hi[3];
+    particle_powers_bbox(ps, n, D, h_powh_.data(), lo, hi);
+    copier.join();
+    CUDA_OK(copy_rc);
     double inv[3];
     for (int a = 0; a < 3; ++a) {
         const double ext = hi[a] - lo[a];
         inv[a] = (ext > 0.0 && std::isfinite(ext)) ? 2097151.0 / ext : 0.0;
         if (!std::isfinite(lo[a])) lo[a] = 0.0;
     }
-    d_raw_.ensure(n * sizeof(sphray_particle));
-    d_powh_raw_.ensure(n * D * sizeof(double));
-    CUDA_OK(cudaMemcpyAsync(d_raw_.p, ps, n * sizeof(sphray_particle), cudaMemcpyHostToDevice, stream_));
-    CUDA_OK(cudaMemcpyAsync(d_powh_raw_.p, h_powh_.data(), n * D * sizeof(double),
-                            cudaMemcpyHostToDevice, stream_));
     d_codes_.ensure(n * 8);
     d_codes2_.ensure(n * 8);
     d_idx_.ensure(n * 4);
@@ -219,6 +224,11 @@ void Engine::upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_
     d_tmp_.ensure(sb);
     cub_sort(d_codes_.as<unsigned long long>(), d_codes2_.as<unsigned long long>(),
              d_idx_.as<uint32_t>(), d_idx2_.as<uint32_t>(), n, 63, d_tmp_.p, d_tmp_.bytes, stream_);
+    // the powers go up while the device sorts
+    CUDA_OK(cudaMemcpyAsync(d_powh_raw_.p, h_powh_.data(), n * D * sizeof(double),
+                            cudaMemcpyHostToDevice, aux_));
+    CUDA_OK(cudaEventRecord(ev_aux_, aux_));
+    CUDA_OK(cudaStreamWaitEvent(stream_, ev_aux_, 0));
     d_pxyzh_.ensure(n * sizeof(double4));
     d_mvr_.ensure(n * sizeof(double4));
     d_powh_.ensure(n * D * sizeof(double));

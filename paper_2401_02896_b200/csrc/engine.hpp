@@ -79,6 +79,8 @@ class Engine {
     int device_ = 0;
     int sm_count_ = 0;
     cudaStream_t stream_ = nullptr;
+    cudaStream_t aux_ = nullptr;  // scene uploads overlapped with host work / device sorts
+    cudaEvent_t ev_aux_ = nullptr;
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, evb_ = nullptr, evr0_ = nullptr, evr1_ = nullptr;
     // communicator (tile gather)
     int rank_ = 0, nranks_ = 1;

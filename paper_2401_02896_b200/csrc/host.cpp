@@ -9,6 +9,7 @@
 #include <numbers>
 #include <random>
 #include <stdexcept>
+#include <mutex>
 #include <thread>
 
 namespace sphray_b200 {
@@ -386,6 +387,37 @@ void particle_powers(const sphray_particle* ps, size_t n, int D, double* out) {
                 last_h = h;
             }
             for (int d = 0; d < D; ++d) out[i * D + d] = last[d];
+        }
+    });
+}
+
+void particle_powers_bbox(const sphray_particle* ps, size_t n, int D, double* out, double lo[3],
+                          double hi[3]) {
+    lo[0] = hi[0] = ps[0].x;
+    lo[1] = hi[1] = ps[0].y;
+    lo[2] = hi[2] = ps[0].z;
+    std::mutex mu;
+    parallel_chunks(n, [&](size_t b, size_t e) {
+        double last_h = std::nan(""), last[kMaxDegree] = {};
+        double l[3] = {ps[b].x, ps[b].y, ps[b].z}, u[3] = {ps[b].x, ps[b].y, ps[b].z};
+        for (size_t i = b; i < e; ++i) {
+            const sphray_particle& p = ps[i];
+            if (!(p.h == last_h)) {
+                for (int d = 1; d <= D; ++d) last[d - 1] = std::pow(p.h, d + 3);  // quantize.hpp:222
+                last_h = p.h;
+            }
+            for (int d = 0; d < D; ++d) out[i * D + d] = last[d];
+            l[0] = std::min(l[0], p.x);
+            l[1] = std::min(l[1], p.y);
+            l[2] = std::min(l[2], p.z);
+            u[0] = std::max(u[0], p.x);
+            u[1] = std::max(u[1], p.y);
+            u[2] = std::max(u[2], p.z);
+        }
+        std::lock_guard<std::mutex> g(mu);
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], l[a]);
+            hi[a] = std::max(hi[a], u[a]);
         }
     });
 }

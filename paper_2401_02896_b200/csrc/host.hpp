@@ -96,6 +96,9 @@ double entry_amplitude(const LutHost& lut, int entry);
 // pow(h, d+3) for d = 1..D per particle (glibc pow, as quantize.hpp:222), the
 // only libm call of quantize that depends on the particle.  Multithreaded.
 void particle_powers(const sphray_particle* ps, size_t n, int D, double* out /* n*D */);
+// the same, plus the coordinate bounding box (lo/hi x, y, z) in the same pass
+void particle_powers_bbox(const sphray_particle* ps, size_t n, int D, double* out, double lo[3],
+                          double hi[3]);
 
 int host_threads();
 
