@@ -203,9 +203,9 @@ void Engine::upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_
             copy_rc = cudaMemcpyAsync(d_raw_.p, ps, n * sizeof(sphray_particle), cudaMemcpyHostToDevice, aux_);
         if (copy_rc == cudaSuccess) copy_rc = cudaStreamSynchronize(aux_);
     });
-    h_powh_.resize(n * D);
+    h_powh_.ensure(n * D * sizeof(double));
     double lo[3], hi[3];
-    particle_powers_bbox(ps, n, D, h_powh_.data(), lo, hi);
+    particle_powers_bbox(ps, n, D, static_cast<double*>(h_powh_.p), lo, hi);
     copier.join();
     CUDA_OK(copy_rc);
     double inv[3];
@@ -225,7 +225,7 @@ void Engine::upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_
     cub_sort(d_codes_.as<unsigned long long>(), d_codes2_.as<unsigned long long>(),
              d_idx_.as<uint32_t>(), d_idx2_.as<uint32_t>(), n, 63, d_tmp_.p, d_tmp_.bytes, stream_);
     // the powers go up while the device sorts
-    CUDA_OK(cudaMemcpyAsync(d_powh_raw_.p, h_powh_.data(), n * D * sizeof(double),
+    CUDA_OK(cudaMemcpyAsync(d_powh_raw_.p, h_powh_.p, n * D * sizeof(double),
                             cudaMemcpyHostToDevice, aux_));
     CUDA_OK(cudaEventRecord(ev_aux_, aux_));
     CUDA_OK(cudaStreamWaitEvent(stream_, ev_aux_, 0));

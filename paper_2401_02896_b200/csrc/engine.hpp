@@ -98,7 +98,7 @@ class Engine {
     DevBuf d_dump_count_, d_dump_hr_, d_dump_hp_, d_dump_hl_, d_dump_ht_, d_dump_pr_, d_dump_pt_,
         d_dump_pa_, d_stats_all_;
     HostPinned h_stage_;
-    std::vector<double> h_powh_;
+    HostPinned h_powh_;  // pow(h, d+3) staging (pinned: the upload is a true async copy)
     long long shape_key_[4] = {-1, -1, -1, -1};  // render CTA shape cache (D, m, tf bytes, window)
     int shape_val_[3] = {0, 0, 0};
     std::vector<double> h_tf_;
