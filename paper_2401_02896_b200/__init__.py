@@ -650,6 +650,12 @@ class Context:
             out[k] = bool(out[k])
         return out
 
+    def upload_file(self, path: str, lut: Lut) -> None:
+        """Loads a particle file (SPRT / CSV) and makes it the resident scene."""
+        err = _Error()
+        _check(self._L.sphray_scene_upload_file(self._h, os.fsencode(path), C.byref(lut.view),
+                                                C.byref(err)), err)
+
     def dataset_stats(self, clustering_factor: float = 16.0) -> DatasetStats:
         """dataset_stats (quantize.hpp:129-165) of the uploaded scene, on the GPU."""
         out, err = _DStats(), _Error()

@@ -378,3 +378,32 @@ def test_alu_peak_probe():
     """The bench's ALU-roofline denominators come from a live probe."""
     pk = S.probe_alu_peaks(0)
     assert 1e3 < pk["int64_gops"] < 1e6 and 1e3 < pk["fp64_gflops"] < 1e6, pk
+
+
+def test_ray_spanning_beyond_32bit_offsets_fails_loudly(ctx):
+    """Knot positions are kept as 32-bit offsets per ray; a ray whose knots
+    span more than 2^32 quanta cannot be represented and must fail with
+    CapacityError (never a wrong image).  (The reference's int64 path throws
+    OverflowError on such a ray: Delta t^D overflows in advance().)"""
+    ps = np.array([[0.0, 0.0, 0.0, 1.0, 1.0, 0.3, 1.0],
+                   [0.0, 0.0, -2.0, 1.0, 1.0, 0.3, 1.0]])
+    lut = S.load_lut(H.lut_path(4, 3, 1024))
+    ds = S.dataset_stats(ps, lut)
+    qc = S.choose_quanta(lut, ds)
+    qc = S.QuantaConfig(1e-10, qc.sigma, 64)
+    cam = S.Camera(**H.synth_camera_kwargs(8, 8))
+    with pytest.raises(S.CapacityError):
+        S.render_scene(ps, cam, S.TransferFunction.from_array(H.SYNTH_TF), lut, qc, ds, ctx=ctx)
+
+
+def test_scene_upload_from_file(ctx, tmp_path):
+    """sphray_scene_upload_file == loading + sphray_scene_upload."""
+    g = load("render_test")
+    lut = S.load_lut(g["lut_path"])
+    path = str(tmp_path / "scene.sprt")
+    S.save_particles(g["particles"], path, binary=True)
+    ctx.upload_file(path, lut)
+    ray, pid, lam, t = ctx.hits(S.Camera(**g["ck"]))
+    o = np.lexsort((g["hit_pidx"], g["hit_ray"]))
+    np.testing.assert_array_equal(pid, g["hit_pidx"][o])
+    np.testing.assert_array_equal(t.view(np.uint64), g["hit_tchi"][o].view(np.uint64))
