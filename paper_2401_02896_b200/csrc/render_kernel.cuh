@@ -144,53 +144,6 @@ __device__ __forceinline__ double alpha_of(double x) {
 }
 
 
-// Warp bitonic sort of 32*R u64 keys held R per lane (blocked layout:
-// element e = lane*R + r), ascending.  The (size, stride) stage loop is a
-// runtime loop so the code stays small (the kernel is instruction-cache
-// sensitive); only the per-register bodies are unrolled.
-template <int R, int J>
-__device__ __forceinline__ void bitonic_intra(uint64_t (&k)[R], int lane, int size) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        if ((r & J) == 0) {
-            const int r2 = r | J;
-            const bool asc = (((lane * R) + r) & size) == 0;
-            const uint64_t a = k[r], b = k[r2];
-            const bool sw = asc ? (a > b) : (a < b);
-            k[r] = sw ? b : a;
-            k[r2] = sw ? a : b;
-        }
-    }
-}
-
-template <int R>
-__device__ __forceinline__ void bitonic_sort(uint64_t (&k)[R], int lane) {
-#pragma unroll 1
-    for (int size = 2; size <= 32 * R; size <<= 1) {
-#pragma unroll 1
-        for (int stride = size >> 1; stride >= 1; stride >>= 1) {
-            if (stride >= R) {
-                const int ls = stride / R;
-                const bool asc = ((lane * R) & size) == 0;
-                const bool keep_min = ((lane & ls) == 0) == asc;
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const uint64_t o = __shfl_xor_sync(kFull, k[r], ls);
-                    k[r] = (keep_min == (o < k[r])) ? o : k[r];
-                }
-            } else if (R > 8 && stride == 8) {
-                bitonic_intra<R, (R > 8 ? 8 : 1)>(k, lane, size);
-            } else if (R > 4 && stride == 4) {
-                bitonic_intra<R, (R > 4 ? 4 : 1)>(k, lane, size);
-            } else if (R > 2 && stride == 2) {
-                bitonic_intra<R, (R > 2 ? 2 : 1)>(k, lane, size);
-            } else {
-                bitonic_intra<R, 1>(k, lane, size);
-            }
-        }
-    }
-}
-
 struct WarpMem {
     uint32_t* pt;    // cap: position offsets (see the file comment)
     uint64_t* pool;  // D x cap: jumps of orders 1..D
