@@ -766,7 +766,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     // sizes that reaches the best warps/SM (windows below ~384 slots make
     // config-3 rays overflow into the retry pass).
     const size_t tfb_full = ntf * kTfPoint * sizeof(double);
-    const size_t tfb = (tfb_full <= 4096 && !std::getenv("SPHRAY_TF_GLOBAL")) ? tfb_full : 0;
+    const size_t tfb = (tfb_full <= 4096 && !dumps && !std::getenv("SPHRAY_TF_GLOBAL")) ? tfb_full : 0;
     P.tf_smem = static_cast<int>(tfb);
     auto best_shape = [&](int cap_, int& warps_, int& bps_) {
         const size_t wb_ = warp_smem_bytes(D, cap_, m);

@@ -180,7 +180,7 @@ __device__ inline WarpMem carve(char* base, int D, int cap) {
 
 // One warp renders one ray at a time.  TS: the transfer function is read
 // from the CTA's shared copy (else from global memory).
-template <int D, int M, bool TS>
+template <int D, int M, bool TS, bool DUMP>
 class RayWorker {
    public:
     static constexpr int KN = 2 * M + 1;  // knots per hit, at most
@@ -350,7 +350,8 @@ class RayWorker {
             tn = more ? pool_t(fs[k + 1]) : t;
             if (more && tn == t) continue;  // more jumps at this position
             ++npc;
-            if (!stop && P.dump_piece_t) dump_piece(t, Pc);
+            if constexpr (DUMP)
+                if (!stop && P.dump_piece_t) dump_piece(t, Pc);
             if (!more) {
                 if (!stop) {
                     w.open[0] = static_cast<uint64_t>(t);
@@ -728,7 +729,7 @@ class RayWorker {
                     w.hq_d2[at] = d2;
                     w.hq_t[at] = tchi;
                 }
-                if (P.dump_hit_ray && m) {
+                if (DUMP && P.dump_hit_ray && m) {
                     unsigned long long base = 0;
                     if (lane == 0)
                         base = atomicAdd(&P.dump_count[0], static_cast<unsigned long long>(__popc(m)));
@@ -822,7 +823,7 @@ class RayWorker {
     }
 };
 
-template <int D, int M, bool TS>
+template <int D, int M, bool TS, bool DUMP>
 __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const FrameParams P) {
     extern __shared__ __align__(16) char smem[];
     const int warp = threadIdx.x >> 5;
@@ -835,7 +836,7 @@ __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const FrameParams P) {
         __syncthreads();
         tf_sa = static_cast<uint32_t>(__cvta_generic_to_shared(st));
     }
-    RayWorker<D, M, TS> rw(P, wm, lane, tf_sa);
+    RayWorker<D, M, TS, DUMP> rw(P, wm, lane, tf_sa);
     while (true) {
         unsigned long long item = 0;
         if (lane == 0) item = atomicAdd(P.work_counter, 1ull);
@@ -915,10 +916,10 @@ __global__ void k_quantize_hits(const QuantParams Q, const sphray_particle* ps, 
 template <int D, int M>
 int render_occupancy_t(int warps, size_t smem) {
     int nb = 0;
-    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(rk::k_render_rays<D, M, true>,
+    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(rk::k_render_rays<D, M, true, false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
-    SPHRAY_RK_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, rk::k_render_rays<D, M, true>,
+    SPHRAY_RK_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, rk::k_render_rays<D, M, true, false>,
                                                                     warps * 32, smem));
     return nb;
 }
@@ -926,7 +927,12 @@ int render_occupancy_t(int warps, size_t smem) {
 template <int D, int M>
 void launch_render_t(const FrameParams& P, int blocks, int warps, cudaStream_t s) {
     const size_t smem = static_cast<size_t>(P.warp_bytes) * warps + P.tf_smem;
-    auto kern = P.tf_smem ? rk::k_render_rays<D, M, true> : rk::k_render_rays<D, M, false>;
+    // validation dumps get their own instantiation so the production kernel
+    // carries no dump code (it is instruction-cache sensitive); dump frames
+    // read the transfer function from global memory
+    const bool dump = P.dump_hit_ray || P.dump_piece_t;
+    auto kern = dump ? rk::k_render_rays<D, M, false, true>
+                     : (P.tf_smem ? rk::k_render_rays<D, M, true, false> : rk::k_render_rays<D, M, false, false>);
     SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
     kern<<<blocks, warps * 32, smem, s>>>(P);
