@@ -178,62 +178,12 @@ __device__ inline WarpMem carve(char* base, int D, int cap) {
     return w;
 }
 
-// One warp renders one ray at a time.  TS: the transfer function is read
-// from the CTA's shared copy (else from global memory).
-template <int D, int M, bool TS, bool DUMP>
-class RayWorker {
-   public:
-    static constexpr int KN = 2 * M + 1;  // knots per hit, at most
+// Piece compositing (composite(), raycast.hpp:356-381), shared by the lane
+// walk and the out-of-line early-termination replay.
+template <int D, bool TS>
+struct Compositor {
     const FrameParams& P;
-    WarpMem w;
-    int lane;
     uint32_t tf_sa;  // shared address of the CTA's TF copy (TS)
-    uint64_t ray_id = 0;
-    // warp-uniform ray state
-    int np = 0, nfree = 0;
-    uint16_t* fs = nullptr;  // flush set of the current flush (w.fl + nfree)
-    int64_t tb = 0;          // position base of pt[]
-    bool has_base = false;
-    uint64_t G[D + 1];  // running sum of jumps shifted to tref (mod 2^64)
-    int64_t tref = 0;
-    bool has_ref = false;
-    bool has_open = false;  // w.open holds the last piece
-    double T = 1.0;
-    double Cr = 0.0, Cg = 0.0, Cb = 0.0;  // per-lane partial colour sums (reduced in finish)
-    bool term = false;
-    unsigned long long knots = 0, pieces = 0, hits = 0;
-    int max_pending = 0;
-    int max_resid = 0;  // SPHRAY_KSTATS: largest pending set left by a flush
-
-    __device__ RayWorker(const FrameParams& p, WarpMem wm, int l, uint32_t t)
-        : P(p), w(wm), lane(l), tf_sa(t) {}
-
-    __device__ __forceinline__ int64_t pool_t(int slot) const {
-        return tb + static_cast<int64_t>(w.pt[slot]);
-    }
-    __device__ __forceinline__ uint64_t& pool_c(int d, int slot) const {
-        return w.pool[(d - 1) * P.cap + slot];
-    }
-
-    __device__ void reset() {
-        np = 0;
-        nfree = P.cap;
-        for (int i = lane; i < P.cap; i += 32) w.fl[i] = static_cast<uint16_t>(P.cap - 1 - i);
-#pragma unroll
-        for (int d = 0; d <= D; ++d) G[d] = 0;
-        tref = 0;
-        has_ref = false;
-        has_open = false;
-        tb = 0;
-        has_base = false;
-        T = 1.0;
-        Cr = Cg = Cb = 0.0;
-        term = false;
-        knots = pieces = hits = 0;
-        max_pending = 0;
-        max_resid = 0;
-        __syncwarp();
-    }
 
     // Samples of one piece, front to back, from transmittance T0 (composite(),
     // raycast.hpp:369-377): midpoints lo + (s + 1/2) dt as the reference
@@ -321,6 +271,114 @@ class RayWorker {
         Tl = To;
     }
 
+};
+
+template <int D>
+struct ReplayIn {
+    uint64_t E[D + 1];   // sum of the jumps before the run, around tref
+    uint64_t oa[D + 1];  // the previous open piece (lead lane)
+    int64_t ot;
+    bool lead;
+    double Tb;  // the run's true starting transmittance
+};
+struct ReplayOut {
+    double T, r, g, b;
+};
+
+// Early-termination replay of one lane's run (raycast.hpp:363, 369): the walk
+// of RayWorker::walk from the true T with the per-sample stop test.  Out of
+// line: it runs at most once per ray, and the render kernel is
+// instruction-cache bound.
+template <int D, bool TS>
+__device__ __noinline__ ReplayOut replay_run(const FrameParams& P, uint32_t tf_sa, const uint16_t* fs,
+                                             const uint32_t* pt, const uint64_t* pool, int cap,
+                                             int64_t tb, int64_t tref, int k0, int k1, int nsel,
+                                             ReplayIn<D> in) {
+    const Compositor<D, TS> cmp{P, tf_sa};
+    double Tl = in.Tb, cr = 0.0, cg = 0.0, cb = 0.0;
+    int nsmp = 0;
+    int64_t tcur = tb + static_cast<int64_t>(pt[fs[k0]]);
+    if (in.lead) cmp.composite_piece(in.ot, tcur, in.oa, true, Tl, cr, cg, cb, nsmp);
+    uint64_t Pc[D + 1];
+#pragma unroll
+    for (int d = 0; d <= D; ++d) Pc[d] = in.E[d];
+    taylor_shift<D>(Pc, static_cast<uint64_t>(tcur) - static_cast<uint64_t>(tref));
+    int64_t tn = tcur;
+    for (int k = k0; k < k1; ++k) {
+        const int s = fs[k];
+        const int64_t t = tn;
+        if (t != tcur) {
+            taylor_shift<D>(Pc, static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur));
+            tcur = t;
+        }
+#pragma unroll
+        for (int d = 1; d <= D; ++d) Pc[d] += pool[(d - 1) * cap + s];
+        const bool more = k + 1 < nsel;
+        tn = more ? tb + static_cast<int64_t>(pt[fs[k + 1]]) : t;
+        if (more && tn != t) cmp.composite_piece(t, tn, Pc, true, Tl, cr, cg, cb, nsmp);
+    }
+    return {Tl, cr, cg, cb};
+}
+
+// One warp renders one ray at a time.  TS: the transfer function is read
+// from the CTA's shared copy (else from global memory).
+template <int D, int M, bool TS, bool DUMP>
+class RayWorker {
+   public:
+    static constexpr int KN = 2 * M + 1;  // knots per hit, at most
+    const FrameParams& P;
+    WarpMem w;
+    int lane;
+    uint32_t tf_sa;  // shared address of the CTA's TF copy (TS)
+    uint64_t ray_id = 0;
+    // warp-uniform ray state
+    int np = 0, nfree = 0;
+    uint16_t* fs = nullptr;  // flush set of the current flush (w.fl + nfree)
+    int64_t tb = 0;          // position base of pt[]
+    bool has_base = false;
+    uint64_t G[D + 1];  // running sum of jumps shifted to tref (mod 2^64)
+    int64_t tref = 0;
+    bool has_ref = false;
+    bool has_open = false;  // w.open holds the last piece
+    double T = 1.0;
+    double Cr = 0.0, Cg = 0.0, Cb = 0.0;  // per-lane partial colour sums (reduced in finish)
+    bool term = false;
+    unsigned long long knots = 0, pieces = 0, hits = 0;
+    int max_pending = 0;
+    int max_resid = 0;  // SPHRAY_KSTATS: largest pending set left by a flush
+
+    Compositor<D, TS> cmp;
+
+    __device__ RayWorker(const FrameParams& p, WarpMem wm, int l, uint32_t t)
+        : P(p), w(wm), lane(l), tf_sa(t), cmp{p, t} {}
+
+    __device__ __forceinline__ int64_t pool_t(int slot) const {
+        return tb + static_cast<int64_t>(w.pt[slot]);
+    }
+    __device__ __forceinline__ uint64_t& pool_c(int d, int slot) const {
+        return w.pool[(d - 1) * P.cap + slot];
+    }
+
+    __device__ void reset() {
+        np = 0;
+        nfree = P.cap;
+        for (int i = lane; i < P.cap; i += 32) w.fl[i] = static_cast<uint16_t>(P.cap - 1 - i);
+#pragma unroll
+        for (int d = 0; d <= D; ++d) G[d] = 0;
+        tref = 0;
+        has_ref = false;
+        has_open = false;
+        tb = 0;
+        has_base = false;
+        T = 1.0;
+        Cr = Cg = Cb = 0.0;
+        term = false;
+        knots = pieces = hits = 0;
+        max_pending = 0;
+        max_resid = 0;
+        __syncwarp();
+    }
+
     // Lane-sequential walk over the sorted flush-set knots [k0, k1) -- the
     // RayAccumulator recurrence (raycast.hpp:206-244) on one lane: Pc enters
     // as the sum of every earlier jump around tref, is moved to each knot by
@@ -334,7 +392,7 @@ class RayWorker {
                          double& cg, double& cb, int& npc, int& nsmp) {
         if (k0 >= k1) return;
         int64_t tcur = pool_t(fs[k0]);
-        if (lead && comp) composite_piece(ot, tcur, oa, stop, Tl, cr, cg, cb, nsmp);
+        if (lead && comp) cmp.composite_piece(ot, tcur, oa, stop, Tl, cr, cg, cb, nsmp);
         taylor_shift<D>(Pc, static_cast<uint64_t>(tcur) - static_cast<uint64_t>(tref));
         int64_t tn = tcur;
         for (int k = k0; k < k1; ++k) {
@@ -359,7 +417,7 @@ class RayWorker {
                     for (int d = 0; d <= D; ++d) w.open[1 + d] = Pc[d];
                 }
             } else if (comp) {
-                composite_piece(t, tn, Pc, stop, Tl, cr, cg, cb, nsmp);
+                cmp.composite_piece(t, tn, Pc, stop, Tl, cr, cg, cb, nsmp);
             }
         }
     }
@@ -458,14 +516,21 @@ class RayWorker {
             if (f < 32) {
                 double T2 = Tb;
                 if (lane == f) {
-                    double r2 = 0.0, g2 = 0.0, b2 = 0.0;
-                    int d1 = 0, d2 = 0;
+                    ReplayIn<D> in;
 #pragma unroll
-                    for (int d = 0; d <= D; ++d) Pc[d] = E[d];
-                    walk(k0, k1, nsel, Pc, true, true, lead, ot, oa, T2, r2, g2, b2, d1, d2);
-                    Cr += r2;
-                    Cg += g2;
-                    Cb += b2;
+                    for (int d = 0; d <= D; ++d) {
+                        in.E[d] = E[d];
+                        in.oa[d] = oa[d];
+                    }
+                    in.ot = ot;
+                    in.lead = lead;
+                    in.Tb = Tb;
+                    const ReplayOut o = replay_run<D, TS>(P, tf_sa, fs, w.pt, w.pool, P.cap, tb, tref, k0,
+                                                          k1, nsel, in);
+                    T2 = o.T;
+                    Cr += o.r;
+                    Cg += o.g;
+                    Cb += o.b;
                 }
                 Tend = __shfl_sync(kFull, T2, f);
                 term = true;
@@ -824,7 +889,7 @@ class RayWorker {
 };
 
 template <int D, int M, bool TS, bool DUMP>
-__global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const FrameParams P) {
+__global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const __grid_constant__ FrameParams P) {
     extern __shared__ __align__(16) char smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
