@@ -775,7 +775,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         bps_ = 0;
         for (int wpb : {4, 2, 8, 1, 3, 6}) {
             if (wb_ * wpb + tfb > kSmemLimit) continue;
-            const int nb = max_blocks_per_sm(D, m, wpb, wb_ * wpb + tfb);
+            const int nb = max_blocks_per_sm(D, m, wpb, wb_ * wpb + tfb, lut_.K % 2 == 0);
             if (nb * wpb > best_) {
                 best_ = nb * wpb;
                 warps_ = wpb;
@@ -787,7 +787,8 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     int cap = 0, warps = 1, bps = 0;
     // validation dumps (hits / pieces) are written as rays run, so a ray must
     // not be re-run: dump frames use the widest window from the start
-    const long long shape_key[4] = {D, m, static_cast<long long>(tfb), dumps ? -1 : opts.window};
+    const long long shape_key[4] = {D * 16 + lut_.K, m, static_cast<long long>(tfb),
+                                    dumps ? -1 : opts.window};
     if (std::equal(shape_key, shape_key + 4, shape_key_)) {
         cap = shape_val_[0];
         warps = shape_val_[1];
@@ -858,7 +859,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         P2.retry_list = d_retry2_.as<uint32_t>();
         P2.retry_count = d_retry_count_.as<unsigned int>() + 1;
         CUDA_OK(cudaMemsetAsync(d_work_.p, 0, 8, s));
-        int bps2 = max_blocks_per_sm(D, m, 1, P2.warp_bytes + tfb);
+        int bps2 = max_blocks_per_sm(D, m, 1, P2.warp_bytes + tfb, lut_.K % 2 == 0);
         if (bps2 < 1) bps2 = 1;
         launch_render(P2, D, m, std::min<int>(retry, sm_count_ * bps2), 1, s);
         ++launches;

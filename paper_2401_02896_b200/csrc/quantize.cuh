@@ -37,15 +37,14 @@ struct HitPositions {
 };
 
 // Phase A.  Returns false when quantize_particle emits nothing (lam >= q,
-// quantize.hpp:204).  All array indices are compile-time (M is a template
-// parameter, the parity of K a runtime select) so nothing spills to local
-// memory.
-template <int M>
+// quantize.hpp:204).  All array indices are compile-time (M and the parity of
+// K are template parameters) so nothing spills to local memory.
+template <int M, bool EVEN>
 __device__ __forceinline__ bool quantize_positions(const QuantParams& Q, double h, double lam,
                                                    double tchi, HitPositions<M>& hp,
                                                    bool& ovf) {
     constexpr int KN = HitPositions<M>::KN;
-    const bool even = (Q.K & 1) == 0;
+    constexpr bool even = EVEN;  // K even (compile time: dead closure code stays out)
     hp.nraw = even ? KN : KN - 1;
     hp.nk = 0;
 #pragma unroll
@@ -82,13 +81,13 @@ __device__ __forceinline__ bool quantize_positions(const QuantParams& Q, double 
 // (quantize.hpp:221-222 with the libm parts precomputed on the host),
 // X[2D..3D) = recip_or_nan(X[D..2D)) for rint_div.
 // sink(o, t, b) receives distinct knot o (0..nk) with its D+1 jumps.
-template <int D, int M, class Sink>
+template <int D, int M, bool EVEN, class Sink>
 __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double* X,
                                               const HitPositions<M>& hp, bool& ovf,
                                               Sink&& sink) {
     constexpr int m = M;
     constexpr int KN = HitPositions<M>::KN;
-    const bool even = (Q.K & 1) == 0;
+    constexpr bool even = EVEN;  // K even (compile time: dead closure code stays out)
     int64_t negk[M][D + 1];  // negk[k-1] == bneg[m-k] of lut.hpp:106
     int64_t center[D + 1];
 #pragma unroll

@@ -225,7 +225,7 @@ __global__ void k_stats_columns(const double4* pxyzh, const double4* mvr, size_t
 
 // defined in render_d<D>.cu (render_kernel.cuh)
 template <int D, int M>
-int render_occupancy_t(int warps, size_t smem);
+int render_occupancy_t(int warps, size_t smem, bool even);
 template <int D, int M>
 void launch_render_t(const FrameParams& P, int blocks, int warps, cudaStream_t s);
 template <int D, int M>
@@ -286,9 +286,9 @@ size_t warp_smem_bytes(int D, int cap, int mm) {
     }
 #endif
 
-int max_blocks_per_sm(int D, int mm, int warps, size_t smem) {
+int max_blocks_per_sm(int D, int mm, int warps, size_t smem, bool even) {
     int nb = 0;
-    SPHRAY_DISPATCH(D, mm, { nb = render_occupancy_t<DD, MM>(warps, smem); });
+    SPHRAY_DISPATCH(D, mm, { nb = render_occupancy_t<DD, MM>(warps, smem, even); });
     return nb;
 }
 

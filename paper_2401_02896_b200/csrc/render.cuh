@@ -143,7 +143,7 @@ struct PrepParams {
 };
 
 size_t warp_smem_bytes(int D, int cap, int m);
-int max_blocks_per_sm(int D, int m, int warps, size_t smem);
+int max_blocks_per_sm(int D, int m, int warps, size_t smem, bool even_k);
 // dataset_stats (quantize.hpp:129-165) of the resident scene: medians of
 // mass, density, h, value (med[0..3]), phi_max, and whether some particle has
 // h <= 0 or density <= 0.

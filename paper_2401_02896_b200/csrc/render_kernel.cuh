@@ -322,7 +322,7 @@ __device__ __noinline__ ReplayOut replay_run(const FrameParams& P, uint32_t tf_s
 
 // One warp renders one ray at a time.  TS: the transfer function is read
 // from the CTA's shared copy (else from global memory).
-template <int D, int M, bool TS, bool DUMP>
+template <int D, int M, bool TS, bool DUMP, bool EVEN>
 class RayWorker {
    public:
     static constexpr int KN = 2 * M + 1;  // knots per hit, at most
@@ -689,7 +689,7 @@ class RayWorker {
         }
         bool ovf = false;
         HitPositions<M> hp;
-        bool emits = act && quantize_positions<M>(P.Q, h, lam, tchi, hp, ovf);
+        bool emits = act && quantize_positions<M, EVEN>(P.Q, h, lam, tchi, hp, ovf);
         int nk = emits ? hp.nk : 0;
         if (ovf) {
             report_overflow(pi);
@@ -713,7 +713,7 @@ class RayWorker {
             const double* xs = P.xy + static_cast<size_t>(pi) * (3 * D);
 #pragma unroll
             for (int d = 0; d < 3 * D; ++d) X[d] = xs[d];
-            quantize_emit<D, M>(P.Q, X, hp, ovf, [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
+            quantize_emit<D, M, EVEN>(P.Q, X, hp, ovf, [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
                 const int slot = w.fl[slot0 + o];
                 // b[0] is structurally zero (lut.hpp:107-166): only orders 1..D are stored
                 const uint64_t to = static_cast<uint64_t>(t) - static_cast<uint64_t>(tb);
@@ -888,7 +888,7 @@ class RayWorker {
     }
 };
 
-template <int D, int M, bool TS, bool DUMP>
+template <int D, int M, bool TS, bool DUMP, bool EVEN>
 __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const __grid_constant__ FrameParams P) {
     extern __shared__ __align__(16) char smem[];
     const int warp = threadIdx.x >> 5;
@@ -901,7 +901,7 @@ __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const __grid_constant_
         __syncthreads();
         tf_sa = static_cast<uint32_t>(__cvta_generic_to_shared(st));
     }
-    RayWorker<D, M, TS, DUMP> rw(P, wm, lane, tf_sa);
+    RayWorker<D, M, TS, DUMP, EVEN> rw(P, wm, lane, tf_sa);
     while (true) {
         unsigned long long item = 0;
         if (lane == 0) item = atomicAdd(P.work_counter, 1ull);
@@ -938,7 +938,7 @@ __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const __grid_constant_
 }
 
 // quantize_particle for explicit hits (validation entry point).
-template <int D, int M>
+template <int D, int M, bool EVEN>
 __global__ void k_quantize_hits(const QuantParams Q, const sphray_particle* ps, const double* powh,
                                 const double* powtau, size_t nhits, const double* tchi,
                                 const double* lam, int64_t* knot_t, int64_t* knot_b,
@@ -949,7 +949,7 @@ __global__ void k_quantize_hits(const QuantParams Q, const sphray_particle* ps, 
     const sphray_particle p = ps[i];
     bool ovf = false;
     HitPositions<M> hp;
-    if (!quantize_positions<M>(Q, p.h, lam[i], tchi[i], hp, ovf)) {
+    if (!quantize_positions<M, EVEN>(Q, p.h, lam[i], tchi[i], hp, ovf)) {
         knot_count[i] = ovf ? -1 : 0;
         return;
     }
@@ -960,7 +960,7 @@ __global__ void k_quantize_hits(const QuantParams Q, const sphray_particle* ps, 
         X[2 * D + d - 1] = recip_or_nan(X[D + d - 1]);
     }
     const int stride = Q.K + 1;
-    quantize_emit<D, M>(Q, X, hp, ovf, [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
+    quantize_emit<D, M, EVEN>(Q, X, hp, ovf, [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
         if (o < KN && o < stride) {
             knot_t[i * stride + o] = t;
             for (int d = 0; d <= D; ++d) knot_b[(i * stride + o) * (D + 1) + d] = b[d];
@@ -978,30 +978,45 @@ __global__ void k_quantize_hits(const QuantParams Q, const sphray_particle* ps, 
             fail(SPHRAY_ERR_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
     } while (0)
 
-template <int D, int M>
-int render_occupancy_t(int warps, size_t smem) {
+template <int D, int M, bool EVEN>
+int render_occupancy_tt(int warps, size_t smem) {
     int nb = 0;
-    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(rk::k_render_rays<D, M, true, false>,
+    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(rk::k_render_rays<D, M, true, false, EVEN>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
-    SPHRAY_RK_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, rk::k_render_rays<D, M, true, false>,
-                                                                    warps * 32, smem));
+    SPHRAY_RK_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &nb, rk::k_render_rays<D, M, true, false, EVEN>, warps * 32, smem));
     return nb;
 }
 
 template <int D, int M>
-void launch_render_t(const FrameParams& P, int blocks, int warps, cudaStream_t s) {
+int render_occupancy_t(int warps, size_t smem, bool even) {
+    return even ? render_occupancy_tt<D, M, true>(warps, smem) : render_occupancy_tt<D, M, false>(warps, smem);
+}
+
+template <int D, int M, bool EVEN>
+void launch_render_tt(const FrameParams& P, int blocks, int warps, cudaStream_t s) {
     const size_t smem = static_cast<size_t>(P.warp_bytes) * warps + P.tf_smem;
     // validation dumps get their own instantiation so the production kernel
     // carries no dump code (it is instruction-cache sensitive); dump frames
     // read the transfer function from global memory
     const bool dump = P.dump_hit_ray || P.dump_piece_t;
-    auto kern = dump ? rk::k_render_rays<D, M, false, true>
-                     : (P.tf_smem ? rk::k_render_rays<D, M, true, false> : rk::k_render_rays<D, M, false, false>);
+    auto kern = dump ? rk::k_render_rays<D, M, false, true, EVEN>
+                     : (P.tf_smem ? rk::k_render_rays<D, M, true, false, EVEN>
+                                  : rk::k_render_rays<D, M, false, false, EVEN>);
     SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
     kern<<<blocks, warps * 32, smem, s>>>(P);
     SPHRAY_RK_CUDA_OK(cudaGetLastError());
+}
+
+// the parity of K selects the closure at compile time (quantize.cuh)
+template <int D, int M>
+void launch_render_t(const FrameParams& P, int blocks, int warps, cudaStream_t s) {
+    if ((P.Q.K & 1) == 0)
+        launch_render_tt<D, M, true>(P, blocks, warps, s);
+    else
+        launch_render_tt<D, M, false>(P, blocks, warps, s);
 }
 
 template <int D, int M>
@@ -1009,13 +1024,18 @@ void launch_quantize_hits_t(const QuantParams& Q, const sphray_particle* ps, con
                             const double* powtau, size_t nhits, const double* tchi,
                             const double* lam, int64_t* knot_t, int64_t* knot_b,
                             int32_t* knot_count, cudaStream_t s) {
-    rk::k_quantize_hits<D, M><<<static_cast<unsigned>((nhits + 127) / 128), 128, 0, s>>>(
-        Q, ps, powh, powtau, nhits, tchi, lam, knot_t, knot_b, knot_count);
+    const unsigned g = static_cast<unsigned>((nhits + 127) / 128);
+    if ((Q.K & 1) == 0)
+        rk::k_quantize_hits<D, M, true><<<g, 128, 0, s>>>(Q, ps, powh, powtau, nhits, tchi, lam,
+                                                           knot_t, knot_b, knot_count);
+    else
+        rk::k_quantize_hits<D, M, false><<<g, 128, 0, s>>>(Q, ps, powh, powtau, nhits, tchi, lam,
+                                                            knot_t, knot_b, knot_count);
     SPHRAY_RK_CUDA_OK(cudaGetLastError());
 }
 
 #define SPHRAY_INSTANTIATE(D, M)                                                             \
-    template int render_occupancy_t<D, M>(int, size_t);                                      \
+    template int render_occupancy_t<D, M>(int, size_t, bool);                                \
     template void launch_render_t<D, M>(const FrameParams&, int, int, cudaStream_t);         \
     template void launch_quantize_hits_t<D, M>(const QuantParams&, const sphray_particle*,   \
                                                const double*, const double*, size_t,         \
