@@ -139,14 +139,22 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
-def setup_scene(cfg, n_override=0):
+def lut_file(args=None):
+    """The LUT of the run: cubic B-spline, K pieces, degree D, 1024 entries
+    (config 4's order sweep varies K and D; every other config is K=4, D=3)."""
+    K = getattr(args, "K", 4) if args is not None else 4
+    D = getattr(args, "D", 3) if args is not None else 3
+    return os.path.join(ROOT, "data", "luts", f"cubic_K{K}_D{D}_N1024.splt")
+
+
+def setup_scene(cfg, n_override=0, args=None):
     import paper_2401_02896_b200 as S
 
     c = CONFIGS[cfg]
     n = n_override or c["n"]
     t0 = time.time()
     ps = S.generate_scene(cfg, n=n)
-    lut = S.load_lut(os.path.join(ROOT, "data", "luts", "cubic_K4_D3_N1024.splt"))
+    lut = S.load_lut(lut_file(args))
     ds = S.dataset_stats(ps, lut)
     qc = S.choose_quanta(lut, ds)
     return ps, lut, ds, qc, time.time() - t0
@@ -201,8 +209,8 @@ def run_reference(args):
         return
     cfg = args.config
     res = args.res or CONFIGS[cfg]["res"]
-    ps, lut, ds, qc, _ = setup_scene(cfg, args.n)
-    lut_path = os.path.join(ROOT, "data", "luts", "cubic_K4_D3_N1024.splt")
+    ps, lut, ds, qc, _ = setup_scene(cfg, args.n, args)
+    lut_path = lut_file(args)
     times = []
     per_step_budget = args.ref_step_budget
     for i in range(args.warmup + args.steps):
@@ -217,7 +225,7 @@ def run_reference(args):
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "impl": "reference",
            "config": {"workload": f"config {cfg}: {CONFIGS[cfg]['desc']}", "particles": len(ps),
-                      "image": f"{res}x{res}", "K": 4, "D": 3, "N_lut": 1024, "int_width": 64},
+                      "image": f"{res}x{res}", "K": args.K, "D": args.D, "N_lut": 1024, "int_width": 64},
            "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": times[0]["cores"],
                             "kind": "reference", "sample": times[0]["sample"]},
            "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0,
@@ -239,7 +247,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = args.config
     res = args.res or CONFIGS[cfg]["res"]
-    ps, lut, ds, qc, setup_s = setup_scene(cfg, args.n)
+    ps, lut, ds, qc, setup_s = setup_scene(cfg, args.n, args)
     ctx = S.Context(local)
     SD.init_comm(ctx, rank, world)
     cam = S.Camera(**camera_kwargs(res))
@@ -355,7 +363,7 @@ def run_ours(args):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                lut_path = os.path.join(ROOT, "data", "luts", "cubic_K4_D3_N1024.splt")
+                lut_path = lut_file(args)
                 cpu = cpu_reference_sample(ps, lut_path, ds, qc, res, budget_s=args.cpu_budget)
                 cpu.pop("seconds", None)
             except Exception as e:  # report, never fake
@@ -367,7 +375,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"config {cfg}: {CONFIGS[cfg]['desc']}",
-                       "particles": len(ps), "image": f"{res}x{res}", "K": 4, "D": 3,
+                       "particles": len(ps), "image": f"{res}x{res}", "K": args.K, "D": args.D,
                        "N_lut": 1024, "int_width": 64, "mode": args.mode,
                        "parallelism": f"image tiles 8x8 interleaved over {world} GPU(s), "
                                       "particles replicated, NCCL tile gather",
@@ -409,6 +417,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-step-budget", type=float, default=5.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--K", type=int, default=4, choices=[1, 2, 3, 4], help="LUT pieces (order sweep)")
+    ap.add_argument("--D", type=int, default=3, choices=[1, 2, 3], help="LUT degree (order sweep)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -186,6 +186,7 @@ void Engine::upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_
     CUDA_OK(cudaMemcpyAsync(d_lut_.p, lut_.rows.data(), lut_.rows.size() * sizeof(double),
                             cudaMemcpyHostToDevice, stream_));
     has_scene_ = true;
+    scene_extent_ = 0.0;
     if (n == 0) {
         CUDA_OK(cudaStreamSynchronize(stream_));
         return;
@@ -208,6 +209,14 @@ void Engine::upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_
     particle_powers_bbox(ps, n, D, static_cast<double*>(h_powh_.p), lo, hi);
     copier.join();
     CUDA_OK(copy_rc);
+    {
+        double hmax = 0.0;
+        for (size_t i = 0; i < n; i += std::max<size_t>(1, n / 65536)) hmax = std::max(hmax, ps[i].h);
+        const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+        scene_extent_ = std::sqrt(dx * dx + dy * dy + dz * dz);
+        if (!std::isfinite(scene_extent_)) scene_extent_ = 1e300;
+        scene_extent_ += 4.0 * hmax * lut_.q;  // knots reach about q h beyond a centre
+    }
     double inv[3];
     for (int a = 0; a < 3; ++a) {
         const double ext = hi[a] - lo[a];
@@ -766,7 +775,14 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     // sizes that reaches the best warps/SM (windows below ~384 slots make
     // config-3 rays overflow into the retry pass).
     const size_t tfb_full = ntf * kTfPoint * sizeof(double);
-    const size_t tfb = (tfb_full <= 4096 && !dumps && !std::getenv("SPHRAY_TF_GLOBAL")) ? tfb_full : 0;
+    // Frames whose rays can span more than ~2^31 position quanta (tiny tau,
+    // e.g. degree-1 tables) run the robust variant from the start: it moves
+    // the 32-bit window-offset base with every flush.  (The hmax sample above
+    // is a heuristic; rays that still overflow go to the robust retry pass.)
+    const bool robust_frame = scene_extent_ / qc.tau > 2147483648.0;
+    P.robust = robust_frame ? 1 : 0;
+    const size_t tfb =
+        (tfb_full <= 4096 && !dumps && !robust_frame && !std::getenv("SPHRAY_TF_GLOBAL")) ? tfb_full : 0;
     P.tf_smem = static_cast<int>(tfb);
     auto best_shape = [&](int cap_, int& warps_, int& bps_) {
         const size_t wb_ = warp_smem_bytes(D, cap_, m);
@@ -855,6 +871,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         P2.cap = cap2;
         P2.warp_bytes = static_cast<int>(warp_smem_bytes(D, cap2, m));
         P2.ray_list = d_retry_.as<uint32_t>();
+        P2.tf_smem = 0;  // the robust retry variant reads the TF from global memory
         P2.total_work = retry;
         P2.retry_list = d_retry2_.as<uint32_t>();
         P2.retry_count = d_retry_count_.as<unsigned int>() + 1;

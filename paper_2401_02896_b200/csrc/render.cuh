@@ -78,6 +78,7 @@ struct FrameParams {
     int cap;         // knot slots per warp
     int warp_bytes;  // dynamic smem per warp
     int tf_smem;     // bytes of the per-CTA shared copy of tf after the windows (0: read global)
+    int robust;      // use the robust variant (rebasing window offsets) for this launch
     // work distribution
     unsigned long long* work_counter;
     uint64_t total_work;

@@ -629,6 +629,13 @@ class RayWorker {
         const uint64_t dF = static_cast<uint64_t>(F) - static_cast<uint64_t>(tb);
         const uint64_t Fo = all_ ? 0x100000000ull
                             : (F <= tb ? 0ull : (dF > 0x100000000ull ? 0x100000000ull : dF));
+        // Robust variant (DUMP): every knot kept pending (and every later one)
+        // is >= F, so the position base moves up to F in this pass and pt[]
+        // offsets only span the live window, not the whole ray (small tau,
+        // long rays).  The set being flushed keeps the old base until merged.
+        const int64_t tb_next = (DUMP && !all_ && F > tb) ? F : tb;
+        const uint32_t keep_shift =
+            (DUMP && Fo > 0 && Fo < 0x100000000ull) ? static_cast<uint32_t>(Fo) : 0u;
         uint32_t tmin = 0xffffffffu, tmax = 0u;
         for (int c0 = 0; c0 < np; c0 += 32) {
             const int i = c0 + lane;
@@ -645,6 +652,7 @@ class RayWorker {
                 tmax = t > tmax ? t : tmax;
             } else if (valid) {
                 w.ps[nkeep + __popc(mkeep & lanemask_lt())] = static_cast<uint16_t>(s);
+                if (keep_shift) w.pt[s] = t - keep_shift;
             }
             nsel += __popc(msel);
             nkeep += __popc(mkeep);
@@ -655,8 +663,10 @@ class RayWorker {
         SPHRAY_KS(kStatSelected, nsel);
         np = nkeep;
         if (SPHRAY_KSTATS && np > max_resid) max_resid = np;
-        if (nsel == 0) return;
-#pragma unroll
+        if (nsel == 0) {
+            tb = tb_next;
+            return;
+        }
         tmin = __reduce_min_sync(kFull, tmin);
         tmax = __reduce_max_sync(kFull, tmax);
         const uint32_t range = tmax - tmin;
@@ -668,6 +678,7 @@ class RayWorker {
         if (nsel > 1) sort_flush_radix(nsel, tmin, bits);
 
         merge_composite(nsel);
+        tb = tb_next;
     }
 
     __device__ void report_overflow(int pi) {
@@ -677,7 +688,9 @@ class RayWorker {
 
     // Quantize the first nq queued hits (lane per hit) and append their knots
     // to the pending list.  Returns false if the window is too small.
-    __device__ bool insert_hits(int nq, int64_t F) {
+    // 0: inserted; 1: the window is full; 2: a position falls outside the
+    // 32-bit offset range of the current base.
+    __device__ int insert_hits(int nq, int64_t F) {
         const bool act = lane < nq;
         int pi = 0;
         double lam = 0.0, tchi = 0.0, h = 0.0;
@@ -699,8 +712,8 @@ class RayWorker {
         const int off = warp_incl_scan(nk, lane) - nk;
         const int total = __shfl_sync(kFull, off + nk, 31);
         SPHRAY_KS(kStatBatches, 1);
-        if (total == 0) return true;
-        if (total > nfree) return false;  // the caller flushed; the window is genuinely full
+        if (total == 0) return 0;
+        if (total > nfree) return 1;  // the caller flushed; the window is genuinely full
         const int slot0 = nfree - total + off;  // this lane's slots: fl[slot0 .. slot0 + nk)
         if (!has_base) {
             // every knot of the ray is >= the current flush bound
@@ -728,13 +741,13 @@ class RayWorker {
         // a ray spanning more than 2^32 position quanta does not fit the
         // 32-bit offsets: treated like a window overflow (retry pass, then
         // CapacityError)
-        if (__any_sync(kFull, far_)) return false;
+        if (__any_sync(kFull, far_)) return 2;
         __syncwarp();
         nfree -= total;
         np += total;
         knots += total;
         if (np > max_pending) max_pending = np;
-        return true;
+        return 0;
     }
 
     // Drop the first nq queued hits (up to 63 queued: shift in chunks of 32).
@@ -819,14 +832,30 @@ class RayWorker {
             // bound of the first hit still queued, or of the next untested
             // candidate (both depth-sorted) -- is final.
             bool stuck = false;
+            int nq_cap = 32;
 #pragma unroll 1
             for (int round = 0; round < SPHRAY_INSERT_ROUNDS && hq_n > 0; ++round) {
-                const int nq = min(min(hq_n, 32), nfree / KN);
+                const int nq = min(min(hq_n, nq_cap), nfree / KN);
                 if (nq == 0) {
                     stuck = round == 0;
                     break;
                 }
-                if (!insert_hits(nq, knot_floor(P.front[w.hq_p[0]], P.Q.tau))) return false;
+                const int64_t F0 = knot_floor(P.front[w.hq_p[0]], P.Q.tau);
+                const int rc = insert_hits(nq, F0);
+                if (rc == 1) return false;
+                if (rc == 2) {
+                    // positions beyond the 32-bit offsets of the base: the
+                    // main pass hands the ray to the robust retry variant,
+                    // which finalises what it can (moving the base up to F0)
+                    // and inserts fewer hits at a time
+                    if (!DUMP) return false;
+                    const int np0 = np;
+                    flush(F0, false);
+                    if (nq == 1 && np == np0) return false;  // no progress possible
+                    nq_cap = max(1, nq / 2);
+                    --round;
+                    continue;
+                }
                 drop_queued(nq, hq_n);
             }
             const bool final_ = hq_n == 0 && cursor >= ce;
@@ -997,11 +1026,12 @@ int render_occupancy_t(int warps, size_t smem, bool even) {
 template <int D, int M, bool EVEN>
 void launch_render_tt(const FrameParams& P, int blocks, int warps, cudaStream_t s) {
     const size_t smem = static_cast<size_t>(P.warp_bytes) * warps + P.tf_smem;
-    // validation dumps get their own instantiation so the production kernel
-    // carries no dump code (it is instruction-cache sensitive); dump frames
-    // read the transfer function from global memory
-    const bool dump = P.dump_hit_ray || P.dump_piece_t;
-    auto kern = dump ? rk::k_render_rays<D, M, false, true, EVEN>
+    // Validation dumps and the retry pass use the robust instantiation (dump
+    // code, per-flush rebasing of the 32-bit window offsets, batch splitting);
+    // the production kernel carries none of it (it is instruction-cache
+    // sensitive).  The robust variant reads the transfer function from global.
+    const bool robust = P.dump_hit_ray || P.dump_piece_t || P.ray_list || P.robust;
+    auto kern = robust ? rk::k_render_rays<D, M, false, true, EVEN>
                      : (P.tf_smem ? rk::k_render_rays<D, M, true, false, EVEN>
                                   : rk::k_render_rays<D, M, false, false, EVEN>);
     SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

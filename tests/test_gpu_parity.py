@@ -407,3 +407,31 @@ def test_scene_upload_from_file(ctx, tmp_path):
     o = np.lexsort((g["hit_pidx"], g["hit_ray"]))
     np.testing.assert_array_equal(pid, g["hit_pidx"][o])
     np.testing.assert_array_equal(t.view(np.uint64), g["hit_tchi"][o].view(np.uint64))
+
+
+@pytest.mark.parametrize("K", [2, 4])
+def test_degree_one_small_tau_live_reference(ctx, K):
+    """D = 1 LUTs give a tiny tau (~1e-9 here), so one ray's knot positions
+    span far more than 2^32 quanta; the window's 32-bit offsets are rebased at
+    every flush and only the live window must fit.  Checked against the live
+    reference (pieces bit-exact, image <= 1e-4, stats exact)."""
+    ps, ck = _blob(3000, 32)
+    path = H.lut_path(K, 1, 1024)
+    lut, rl = S.load_lut(path), ref.Lut(path)
+    ds = S.dataset_stats(ps, lut)
+    qc = S.choose_quanta(lut, ds)
+    assert qc.tau < 1e-8
+    rqc = ref.RpQuanta(qc.tau, qc.sigma, 64)
+    ctx.upload(ps, lut)
+    p = ctx.pieces(S.Camera(**ck), qc)
+    r = ref.pipeline(ps, ref.Camera(**ck), rl, rqc)
+    np.testing.assert_array_equal(p["rays"], r["rays"])
+    np.testing.assert_array_equal(p["piece_t"], r["piece_t"])
+    np.testing.assert_array_equal(p["piece_a"], r["piece_a"])
+    img, st = S.render_scene(ps, S.Camera(**ck), S.TransferFunction.from_array(H.SYNTH_TF), lut, qc,
+                             ds, S.RenderOptions(mode=S.MODE_EXACT), ctx=ctx)
+    rgb, rst, _, _ = ref.render_robust(ps, ref.Camera(**ck), H.SYNTH_TF, rl, rqc,
+                                       ref.dataset_stats(ps, rl))
+    assert np.abs(img.pixels - rgb).max() <= RGB_TOL
+    for k in ("knots", "rays_touched", "int_ops", "residual_failures"):
+        assert getattr(st, k) == rst[k], k
