@@ -9,12 +9,12 @@
 //
 // Reference path replaced (all under /root/reference/proj/include/sphray):
 //   particle_ray_footprint  raycast.hpp:128-184   -> k_prep (bbox) + tile binning + gather
-//   detail::hit_ray         raycast.hpp:111-120   -> dev::hit_ray
+//   detail::hit_ray         raycast.hpp:111-120   -> dev::hit_test + dev::lam_of
 //   quantize_particle<Int>  quantize.hpp:199-250  -> quantize.cuh phases A/B
 //   mirror_closure<T>       lut.hpp:100-168       -> quantize.cuh
-//   sort_knots              raycast.hpp:188-194   -> warp bitonic + in-place window merge
-//   accumulate/RayAccumulator raycast.hpp:206-292 -> RayWorker::flush (wrapping-u64 scan)
-//   composite/evaluate_piece/TransferFunction::sample raycast.hpp:295-381 -> composite_chunk
+//   sort_knots              raycast.hpp:188-194   -> flush-set select + warp radix sort
+//   accumulate/RayAccumulator raycast.hpp:206-292 -> RayWorker::merge_composite / walk
+//   composite/evaluate_piece/TransferFunction::sample raycast.hpp:295-381 -> Compositor
 //   render_scene            raycast.hpp:414-497   -> k_render_rays + engine.cpp
 #include <cuda_runtime.h>
 
