@@ -76,8 +76,11 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // floor(front / tau) - 2: every knot of a not-yet-inserted candidate has
 // t >= this (front is a conservative bound, see dev::front_bound).
-__device__ __forceinline__ int64_t knot_floor(float front, double tau) {
-    const double v = floor(static_cast<double>(front) / tau) - 2.0;
+__device__ __forceinline__ int64_t knot_floor(float front, double inv_tau) {
+    // a multiply by 1/tau (relative error ~2^-52) instead of the division:
+    // the bound only has to stay below the knots, one more unit of slack
+    // covers the rounding for |v| < 2^52
+    const double v = floor(static_cast<double>(front) * inv_tau) - 3.0;
     if (!(v > -9.2e18)) return INT64_MIN;
     if (!(v < 9.2e18)) return INT64_MAX;
     return static_cast<int64_t>(v);
@@ -840,7 +843,7 @@ class RayWorker {
                     stuck = round == 0;
                     break;
                 }
-                const int64_t F0 = knot_floor(P.front[w.hq_p[0]], P.Q.tau);
+                const int64_t F0 = knot_floor(P.front[w.hq_p[0]], P.inv_tau);
                 const int rc = insert_hits(nq, F0);
                 if (rc == 1) return false;
                 if (rc == 2) {
@@ -862,7 +865,7 @@ class RayWorker {
             int64_t F = INT64_MAX;
             if (!final_) {
                 const uint32_t pn = hq_n > 0 ? static_cast<uint32_t>(w.hq_p[0]) : P.cand[cursor];
-                F = knot_floor(P.front[pn], P.Q.tau);
+                F = knot_floor(P.front[pn], P.inv_tau);
             }
             if (final_ || stuck || nfree < 32 * KN || np >= (P.cap * SPHRAY_FLUSH_AT) / 8) {
                 const int np0 = np;
