@@ -789,7 +789,10 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         int best_ = 0;
         warps_ = 1;
         bps_ = 0;
+        const char* wenv = std::getenv("SPHRAY_WPB");  // diagnostics: force warps per CTA
+        const int wforce = wenv ? std::atoi(wenv) : 0;
         for (int wpb : {4, 2, 8, 1, 3, 6}) {
+            if (wforce > 0 && wpb != wforce) continue;
             if (wb_ * wpb + tfb > kSmemLimit) continue;
             const int nb = max_blocks_per_sm(D, m, wpb, wb_ * wpb + tfb, lut_.K % 2 == 0);
             if (nb * wpb > best_) {
