@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define SPHRAY_GPU_ABI_VERSION 1
+#define SPHRAY_GPU_ABI_VERSION 2
 
 /* errors.hpp:12-69 -> status codes.  CLI exit codes (sphray_main.cpp:442-462)
  * map CONFIG/IO -> 2, OVERFLOW -> 3, NUMERIC -> 4. */
@@ -124,8 +124,41 @@ typedef struct sphray_render_stats {
     double device_ms;         /* device time of the whole frame (CUDA events) */
     double bin_ms;            /* particle prep + tile binning (sort) */
     double render_ms;         /* the render kernel(s): gather, quantize, merge, composite */
-    uint64_t launches;        /* kernels launched for the frame (ours + CUB's) */
+    uint64_t launches;        /* kernels launched for the frame */
+    uint64_t terminated_rays; /* rays whose transmittance reached <= 1e-3 (early termination) */
 } sphray_render_stats;
+
+/* Per-ray record of a frame rendered with records enabled
+ * (sphray_context_set_rows): the RenderStats counters of one ray
+ * (raycast.hpp:400-408, 471-493) and an order-independent checksum of its
+ * merged FieldPieces (raycast.hpp:198-202, accumulate 261-292): the wrapping
+ * uint64 sum over the ray's pieces of sphray_piece_mix(t, a, D).  In MODE_FAST
+ * the counters of an early-terminated ray cover only the traversed part. */
+typedef struct sphray_ray_record {
+    uint64_t piece_checksum;
+    uint32_t knots;   /* knots emitted on the ray (after the coincident merge) */
+    uint32_t pieces;  /* distinct knot positions = FieldPieces */
+    uint32_t hits;    /* (ray, particle) pairs passing hit_ray */
+    uint32_t flags;   /* SPHRAY_RAY_* */
+} sphray_ray_record;
+#define SPHRAY_RAY_TOUCHED 1u     /* at least one knot */
+#define SPHRAY_RAY_RESIDUAL 2u    /* trailing piece nonzero (residual_failures) */
+#define SPHRAY_RAY_TERMINATED 4u  /* transmittance reached <= 1e-3 */
+
+/* The piece hash of sphray_ray_record.piece_checksum: piece position t and
+ * coefficients a_0..a_D. */
+static inline uint64_t sphray_piece_mix(int64_t t, const int64_t* a, int D) {
+    static const uint64_t M[8] = {0x9E3779B97F4A7C15ull, 0xC2B2AE3D27D4EB4Full,
+                                  0x165667B19E3779F9ull, 0x27D4EB2F165667C5ull,
+                                  0x94D049BB133111EBull, 0xBF58476D1CE4E5B9ull,
+                                  0xD6E8FEB86659FD93ull, 0xFF51AFD7ED558CCDull};
+    uint64_t x = (uint64_t)t * M[0];
+    for (int d = 0; d <= D; ++d) x += (uint64_t)a[d] * M[d + 1];
+    x ^= x >> 31;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 29;
+    return x;
+}
 
 /* OverflowError carries particle index and ray id (errors.hpp:54-63). */
 typedef struct sphray_error {
@@ -169,6 +202,21 @@ sphray_status sphray_context_init_comm(sphray_context* ctx, int rank, int nranks
 sphray_status sphray_context_set_shard(sphray_context* ctx, int rank, int nranks,
                                        sphray_error* err);
 
+/* Pixel region (no reference counterpart; used to check the benchmarked frame
+ * against the reference's own sweep functions): subsequent renders of `ctx`
+ * (sphray_scene_render, sphray_scene_hits, sphray_scene_pieces) trace only
+ * the pixels px in [x0, x0 + w), py in [y0, y0 + h) of the camera -- the same
+ * rays, bit for bit, as the full frame -- and sphray_scene_render writes
+ * h * W * 3 doubles (rows y0 .. y0 + h - 1; pixels outside the region keep the
+ * background).  w == 0 or h == 0 restores full frames.  record_rays != 0
+ * makes every render also keep one sphray_ray_record per pixel of the region
+ * (or frame), row-major over the region, fetched with sphray_context_ray_records.
+ * Single-rank contexts only. */
+sphray_status sphray_context_set_region(sphray_context* ctx, int32_t x0, int32_t y0, int32_t w,
+                                        int32_t h, int32_t record_rays, sphray_error* err);
+sphray_status sphray_context_ray_records(sphray_context* ctx, sphray_ray_record* out, size_t cap,
+                                         size_t* count, sphray_error* err);
+
 /* -------------------------------------------------------------------------
  * Drop-in for  template<class Int> Image render_scene(particles, cam, tf, lut,
  * qc, stats, opts, RenderStats*)   raycast.hpp:414-497.
@@ -195,6 +243,11 @@ sphray_status sphray_scene_render(sphray_context* ctx, const sphray_camera* cam,
                                   const sphray_render_options* opts, double* rgb_out,
                                   sphray_render_stats* out_stats, sphray_error* err);
 const double* sphray_scene_device_image(sphray_context* ctx);
+/* The resident scene: particle count and the LUT's K and D (piece_a of
+ * sphray_scene_pieces holds D + 1 coefficients per piece).  ConfigError when
+ * no scene is uploaded. */
+sphray_status sphray_scene_info(sphray_context* ctx, size_t* n, int32_t* K, int32_t* D,
+                                sphray_error* err);
 
 /* The context's CUDA stream (cudaStream_t), for callers that time or order
  * work around the library's launches. */

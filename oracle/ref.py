@@ -58,6 +58,15 @@ class RpRStats(C.Structure):
         ("step", C.c_double)]
 
 
+class RpRayRecord(C.Structure):
+    _fields_ = [("piece_checksum", C.c_uint64), ("knots", C.c_uint32), ("pieces", C.c_uint32),
+                ("hits", C.c_uint32), ("flags", C.c_uint32)]
+
+
+RAY_RECORD_DTYPE = np.dtype([("piece_checksum", "<u8"), ("knots", "<u4"), ("pieces", "<u4"),
+                             ("hits", "<u4"), ("flags", "<u4")])
+
+
 class RpError(C.Structure):
     _fields_ = [("code", C.c_int), ("particle_index", C.c_int64), ("ray_id", C.c_uint64),
                 ("msg", C.c_char * 256)]
@@ -89,9 +98,12 @@ def lib():
         _lib.rp_lut_load.argtypes = [C.c_char_p, C.POINTER(RpError)]
         _lib.rp_lut_free.argtypes = [C.c_void_p]
         _lib.rp_pipeline_run.restype = C.c_void_p
+        _lib.rp_pipeline_run_region.restype = C.c_void_p
         _lib.rp_footprint.restype = C.c_int64
+        _lib.rp_footprint_region.restype = C.c_int64
         _lib.rp_load_particles.restype = C.c_int64
         _lib.rp_load_tf.restype = C.c_int64
+        _lib.rp_scene_default_count.restype = C.c_size_t
     return _lib
 
 
@@ -241,13 +253,15 @@ def render_robust(particles, cam, tf, lut, qc, ds, step=0.0, background=(0, 0, 0
         return render(particles, cam, tf, lut, qc, ds, step, background, threads, 128) + (128,)
 
 
-def footprint(particles, cam: Camera, q: float):
-    """All hits (ray id, particle index, lam, t_chi), particle-major, reference order."""
+def footprint(particles, cam: Camera, q: float, region=(0, 0, 0, 0)):
+    """All hits (ray id, particle index, lam, t_chi), particle-major, reference order;
+    `region` (x0, y0, w, h) keeps only hits on those pixels (w == 0: the frame)."""
     a = as_particles(particles)
     c = cam.c()
     err = RpError()
-    n = lib().rp_footprint(_pp(a), C.c_size_t(len(a)), C.byref(c), C.c_double(q), None, None,
-                           None, None, C.c_size_t(0), C.byref(err))
+    R = [int(v) for v in region]
+    n = lib().rp_footprint_region(_pp(a), C.c_size_t(len(a)), C.byref(c), C.c_double(q), *R,
+                                  None, None, None, None, C.c_size_t(0), C.byref(err))
     if n < 0:
         raise RefError(err)
     ray = np.zeros(n, np.uint64)
@@ -255,9 +269,9 @@ def footprint(particles, cam: Camera, q: float):
     lam = np.zeros(n, np.float64)
     tchi = np.zeros(n, np.float64)
     P = lambda x, t: x.ctypes.data_as(C.POINTER(t))  # noqa: E731
-    n2 = lib().rp_footprint(_pp(a), C.c_size_t(len(a)), C.byref(c), C.c_double(q),
-                            P(ray, C.c_uint64), P(pidx, C.c_int64), P(lam, C.c_double),
-                            P(tchi, C.c_double), C.c_size_t(n), C.byref(err))
+    n2 = lib().rp_footprint_region(_pp(a), C.c_size_t(len(a)), C.byref(c), C.c_double(q), *R,
+                                   P(ray, C.c_uint64), P(pidx, C.c_int64), P(lam, C.c_double),
+                                   P(tchi, C.c_double), C.c_size_t(n), C.byref(err))
     assert n2 == n
     return ray, pidx, lam, tchi
 
@@ -306,13 +320,16 @@ def composite(piece_t, piece_a, qc: RpQuanta, D: int, tf, step: float, t_min: fl
     return tuple(out)
 
 
-def pipeline(particles, cam: Camera, lut: Lut, qc: RpQuanta, threads: int = 0):
-    """Sweeps 1-2 + accumulate<Int128>: dict of CSR arrays (rays, knots, pieces, ops)."""
+def pipeline(particles, cam: Camera, lut: Lut, qc: RpQuanta, threads: int = 0,
+             region=(0, 0, 0, 0)):
+    """Sweeps 1-2 + accumulate<Int128>: dict of CSR arrays (rays, knots, pieces, ops);
+    `region` (x0, y0, w, h) restricts the rays to those pixels (w == 0: the frame)."""
     a = as_particles(particles)
     c = cam.c()
     err = RpError()
-    h = lib().rp_pipeline_run(_pp(a), C.c_size_t(len(a)), C.byref(c), C.c_void_p(lut.h),
-                              C.byref(qc), threads, C.byref(err))
+    R = [int(v) for v in region]
+    h = lib().rp_pipeline_run_region(_pp(a), C.c_size_t(len(a)), C.byref(c), C.c_void_p(lut.h),
+                                     C.byref(qc), threads, *R, C.byref(err))
     if not h:
         raise RefError(err)
     try:
@@ -386,3 +403,68 @@ def load_camera(path: str) -> Camera:
                   look_at=tuple(c.look_at), up=tuple(c.up), width=c.width, height=c.height,
                   fov_deg=c.fov_deg, ortho_height=c.ortho_height, near=c.near_plane,
                   far=c.far_plane)
+
+
+def render_region(particles, cam: Camera, tf, lut: Lut, qc: RpQuanta, step: float, x0: int,
+                  y0: int, w: int, h: int, background=(0.0, 0.0, 0.0), threads: int = 0,
+                  allow_fallback=True):
+    """Pixels [x0, x0+w) x [y0, y0+h) of the full-frame render_scene through the
+    reference's own sweep functions on the same camera (rp_render_region): returns
+    (rgb of rows y0..y0+h-1 (h, W, 3), per-pixel records (RAY_RECORD_DTYPE, row-major
+    over the region), stats dict, seconds of the reference sweeps, accumulator bits)."""
+    a = as_particles(particles)
+    c = cam.c()
+    tfa, ntf = _tf(tf)
+    y0c = max(0, min(y0, cam.height))
+    y1c = max(y0c, min(y0 + h, cam.height))
+    x0c = max(0, min(x0, cam.width))
+    x1c = max(x0c, min(x0 + w, cam.width))
+    rgb = np.zeros((y1c - y0c, cam.width, 3), np.float64)
+    rec = np.zeros((y1c - y0c) * (x1c - x0c), RAY_RECORD_DTYPE)
+    st, err, sec, bits = RpRStats(), RpError(), C.c_double(), C.c_int()
+    bg = (C.c_double * 3)(*background)
+    _check(lib().rp_render_region(_pp(a), C.c_size_t(len(a)), C.byref(c), tfa, C.c_size_t(ntf),
+                                  C.c_void_p(lut.h), C.byref(qc), C.c_double(step), bg, threads,
+                                  x0, y0, w, h, int(bool(allow_fallback)),
+                                  rgb.ctypes.data_as(C.POINTER(C.c_double)),
+                                  rec.ctypes.data_as(C.c_void_p), C.byref(st), C.byref(sec),
+                                  C.byref(bits), C.byref(err)), err)
+    stats = {f: getattr(st, f) for f, _ in RpRStats._fields_}
+    return rgb, rec, stats, sec.value, bits.value
+
+
+def render_rows(particles, cam: Camera, tf, lut: Lut, qc: RpQuanta, step: float, row0: int,
+                nrows: int, background=(0.0, 0.0, 0.0), threads: int = 0, allow_fallback=True):
+    """Full-width rows [row0, row0+nrows): render_region over those rows."""
+    return render_region(particles, cam, tf, lut, qc, step, 0, row0, cam.width, nrows,
+                         background, threads, allow_fallback)
+
+
+def generate_scene(config: int, n: int = 0, seed=None) -> np.ndarray:
+    """The synthetic scenes of BASELINE.json (include/sphray_scenes.hpp, compiled into
+    oracle/_ref): byte-identical to the product's sphray_generate_scene."""
+    if seed is None:
+        seed = 7 if config in (3, 5) else 42
+    if n == 0:
+        n = lib().rp_scene_default_count(int(config))
+    out = np.zeros((n, 7), np.float64)
+    err = RpError()
+    _check(lib().rp_generate_scene(int(config), C.c_size_t(n), C.c_uint64(seed), _pp(out),
+                                   C.byref(err)), err)
+    return out
+
+
+def piece_mix(t, a, D: int) -> np.ndarray:
+    """sphray_piece_mix (include/sphray_gpu.h) vectorised over pieces (t (P,), a (P, >=D+1))."""
+    M = np.array([0x9E3779B97F4A7C15, 0xC2B2AE3D27D4EB4F, 0x165667B19E3779F9,
+                  0x27D4EB2F165667C5, 0x94D049BB133111EB, 0xBF58476D1CE4E5B9,
+                  0xD6E8FEB86659FD93, 0xFF51AFD7ED558CCD], dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        x = np.asarray(t, np.int64).view(np.uint64) * M[0]
+        A = np.asarray(a, np.int64).view(np.uint64)
+        for d in range(D + 1):
+            x = x + A[:, d] * M[d + 1]
+        x = x ^ (x >> np.uint64(31))
+        x = x * np.uint64(0xBF58476D1CE4E5B9)
+        x = x ^ (x >> np.uint64(29))
+    return x

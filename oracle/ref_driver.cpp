@@ -29,6 +29,7 @@
 
 #include "sphray/io.hpp"
 #include "sphray/raycast.hpp"
+#include "sphray_scenes.hpp"
 
 using namespace sphray;
 
@@ -63,6 +64,11 @@ typedef struct {
     std::uint64_t particles, skipped_particles, knots, rays_touched, int_ops, residual_failures;
     double step;
 } rp_rstats;
+
+typedef struct {
+    std::uint64_t piece_checksum;  // sum of piece_mix over the ray's FieldPieces
+    std::uint32_t knots, pieces, hits, flags;  // flags: 1 touched, 2 residual, 4 T <= 1e-3
+} rp_ray_record;
 
 typedef struct {
     int code;  // 0 ok, 1 config, 2 io, 3 overflow, 4 numeric, 5 other
@@ -209,10 +215,68 @@ struct Pipeline {
     std::vector<std::uint64_t> ray_ops;       // int_ops per ray (Int128 path)
 };
 
+
+// The piece hash of sphray_ray_record.piece_checksum (include/sphray_gpu.h,
+// sphray_piece_mix), restated here so the checker does not include product code.
+std::uint64_t piece_mix(std::int64_t t, const std::int64_t* a, int D) {
+    static const std::uint64_t M[8] = {0x9E3779B97F4A7C15ull, 0xC2B2AE3D27D4EB4Full,
+                                       0x165667B19E3779F9ull, 0x27D4EB2F165667C5ull,
+                                       0x94D049BB133111EBull, 0xBF58476D1CE4E5B9ull,
+                                       0xD6E8FEB86659FD93ull, 0xFF51AFD7ED558CCDull};
+    std::uint64_t x = static_cast<std::uint64_t>(t) * M[0];
+    for (int d = 0; d <= D; ++d) x += static_cast<std::uint64_t>(a[d]) * M[d + 1];
+    x ^= x >> 31;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 29;
+    return x;
+}
+
+// A pixel region [x0, x0 + w) x [y0, y0 + h) of the camera (w == 0: the frame).
+struct Region {
+    int x0 = 0, y0 = 0, x1 = 0, y1 = 0;  // exclusive ends
+    bool contains(int px, int py) const { return px >= x0 && px < x1 && py >= y0 && py < y1; }
+};
+
+Region make_region(const Camera& cam, int x0, int y0, int w, int h) {
+    Region r;
+    if (w <= 0 || h <= 0) {
+        r.x1 = cam.width;
+        r.y1 = cam.height;
+        return r;
+    }
+    r.x0 = std::max(0, std::min(x0, cam.width));
+    r.y0 = std::max(0, std::min(y0, cam.height));
+    r.x1 = std::max(r.x0, std::min(x0 + w, cam.width));
+    r.y1 = std::max(r.y0, std::min(y0 + h, cam.height));
+    return r;
+}
+
+// The reference's conservative orthographic pixel bbox (raycast.hpp:136-149,
+// same operations), used only to skip particles that cannot reach a region;
+// pinhole cameras keep every particle.  Two pixels of slack on each side:
+// this filter is the harness's, not the reference's.
+bool may_reach(const Particle& p, const Camera& cam, double q, const Region& r) {
+    if (cam.mode != Camera::Mode::orthographic) return true;
+    const Vec3 chi{p.x, p.y, p.z};
+    const double support = q * p.h;
+    const Vec3 rel = chi - cam.position;
+    const double hw = 0.5 * cam.ortho_height * cam.aspect();
+    const double hh = 0.5 * cam.ortho_height;
+    const double cx = rel.dot(cam.right());
+    const double cy = rel.dot(cam.up_vector());
+    const double x0 = std::floor((cx - support + hw) / (2 * hw) * cam.width - 0.5) - 1;
+    const double x1 = std::ceil((cx + support + hw) / (2 * hw) * cam.width - 0.5) + 1;
+    const double y0 = std::floor((hh - (cy + support)) / (2 * hh) * cam.height - 0.5) - 1;
+    const double y1 = std::ceil((hh - (cy - support)) / (2 * hh) * cam.height - 0.5) + 1;
+    if (!(x0 == x0 && x1 == x1 && y0 == y0 && y1 == y1)) return true;
+    return !(y1 + 2 < r.y0 || y0 - 2 > r.y1 - 1 || x1 + 2 < r.x0 || x0 - 2 > r.x1 - 1);
+}
+
 template <class Int>
 void collect_knots(std::span<const Particle> ps, const Camera& cam, const Lut& lut,
                    const QuantaConfig& qc, std::vector<QuantizedKnot<Int>>& knots,
-                   int threads, const std::vector<std::uint8_t>* row_mask) {
+                   int threads, const std::vector<std::uint8_t>* row_mask,
+                   const Region* region = nullptr) {
     const int nthreads = resolve_threads(threads);
     std::vector<std::vector<QuantizedKnot<Int>>> buffers(ps.size() ? nthreads : 0);
     if (!ps.empty()) {
@@ -221,9 +285,11 @@ void collect_knots(std::span<const Particle> ps, const Camera& cam, const Lut& l
             const std::size_t lo = b * chunk;
             const std::size_t hi = std::min(lo + chunk, ps.size());
             for (std::size_t i = lo; i < hi; ++i) {
+                if (region && !may_reach(ps[i], cam, lut.q, *region)) continue;
                 auto hits = particle_ray_footprint(ps[i], cam, lut.q);
                 for (const auto& hit : hits) {
                     if (row_mask && !(*row_mask)[hit.ray.py]) continue;
+                    if (region && !region->contains(hit.ray.px, hit.ray.py)) continue;
                     auto ks = quantize_particle<Int>(ps[i], hit.ray.id, hit.t_chi, hit.lam, lut,
                                                      qc, static_cast<std::int64_t>(i));
                     buffers[b].insert(buffers[b].end(), ks.begin(), ks.end());
@@ -363,15 +429,23 @@ int rp_render(const rp_particle* ps, std::size_t n, const rp_camera* c, const rp
 
 // All (ray, particle) hits, particle-major in reference order.  Returns the
 // total count; arrays are filled up to cap.
-std::int64_t rp_footprint(const rp_particle* ps, std::size_t n, const rp_camera* c, double q,
-                          std::uint64_t* ray, std::int64_t* pidx, double* lam, double* tchi,
-                          std::size_t cap, rp_error* err) {
+// rp_footprint_region keeps only hits whose pixel lies in the region
+// (x0, y0, w, h; w == 0: the whole frame).
+std::int64_t rp_footprint_region(const rp_particle* ps, std::size_t n, const rp_camera* c, double q,
+                                 int x0, int y0, int w, int h, std::uint64_t* ray,
+                                 std::int64_t* pidx, double* lam, double* tchi, std::size_t cap,
+                                 rp_error* err) {
     std::int64_t total = 0;
     const int rc = guarded(err, [&] {
         const Camera cam = to_cam(c);
+        const Region reg = make_region(cam, x0, y0, w, h);
+        const bool all = w <= 0 || h <= 0;
         for (std::size_t i = 0; i < n; ++i) {
-            const auto hits = particle_ray_footprint(reinterpret_cast<const Particle*>(ps)[i], cam, q);
+            const Particle& p = reinterpret_cast<const Particle*>(ps)[i];
+            if (!all && !may_reach(p, cam, q, reg)) continue;
+            const auto hits = particle_ray_footprint(p, cam, q);
             for (const auto& h : hits) {
+                if (!all && !reg.contains(h.ray.px, h.ray.py)) continue;
                 if (static_cast<std::size_t>(total) < cap) {
                     ray[total] = h.ray.id;
                     pidx[total] = static_cast<std::int64_t>(i);
@@ -383,6 +457,12 @@ std::int64_t rp_footprint(const rp_particle* ps, std::size_t n, const rp_camera*
         }
     });
     return rc ? -1 : total;
+}
+
+std::int64_t rp_footprint(const rp_particle* ps, std::size_t n, const rp_camera* c, double q,
+                          std::uint64_t* ray, std::int64_t* pidx, double* lam, double* tchi,
+                          std::size_t cap, rp_error* err) {
+    return rp_footprint_region(ps, n, c, q, 0, 0, 0, 0, ray, pidx, lam, tchi, cap, err);
 }
 
 int rp_quantize(const rp_particle* p, std::uint64_t ray, double tchi, double lam, void* lutp,
@@ -450,8 +530,9 @@ int rp_composite(const std::int64_t* piece_t, const std::int64_t* piece_a, std::
 }
 
 // Sweeps 1-3 with intermediate results kept (validation oracle).
-void* rp_pipeline_run(const rp_particle* ps, std::size_t n, const rp_camera* c, void* lutp,
-                      const rp_quanta* q, int threads, rp_error* err) {
+void* rp_pipeline_run_region(const rp_particle* ps, std::size_t n, const rp_camera* c, void* lutp,
+                             const rp_quanta* q, int threads, int x0, int y0, int w, int h,
+                             rp_error* err) {
     auto pl = std::make_unique<Pipeline>();
     const int rc = guarded(err, [&] {
         const Camera cam = to_cam(c);
@@ -460,8 +541,10 @@ void* rp_pipeline_run(const rp_particle* ps, std::size_t n, const rp_camera* c, 
         const QuantaConfig qc = to_qc(q);
         const int D = lut.D;
         pl->D = D;
+        const Region reg = make_region(cam, x0, y0, w, h);
         std::vector<QuantizedKnot<Int128>> knots;
-        collect_knots<Int128>(to_span(ps, n), cam, lut, qc, knots, threads, nullptr);
+        collect_knots<Int128>(to_span(ps, n), cam, lut, qc, knots, threads, nullptr,
+                              (w > 0 && h > 0) ? &reg : nullptr);
         sort_knots(knots);
         std::vector<std::size_t> starts;
         for (std::size_t i = 0; i < knots.size(); ++i)
@@ -502,6 +585,11 @@ void* rp_pipeline_run(const rp_particle* ps, std::size_t n, const rp_camera* c, 
     });
     if (rc) return nullptr;
     return pl.release();
+}
+
+void* rp_pipeline_run(const rp_particle* ps, std::size_t n, const rp_camera* c, void* lutp,
+                      const rp_quanta* q, int threads, rp_error* err) {
+    return rp_pipeline_run_region(ps, n, c, lutp, q, threads, 0, 0, 0, 0, err);
 }
 
 void rp_pipeline_sizes(void* h, std::uint64_t* nrays, std::uint64_t* nknots,
@@ -581,6 +669,150 @@ int rp_render_banded(const rp_particle* ps, std::size_t n, const rp_camera* c,
             run(std::type_identity<std::int64_t>{});
     });
 }
+
+
+// Pixels [x0, x0 + w) x [y0, y0 + h) of the full-frame render_scene, driven
+// only by the reference's public functions on the SAME camera (so the rays are
+// the frame's, bit for bit): particle_ray_footprint -> quantize_particle ->
+// sort_knots -> accumulate -> composite, with render_scene's pixel formula
+// (raycast.hpp:466-488).  Particles whose reference bbox misses the region are
+// skipped first (may_reach; orthographic cameras only).  Outputs rows
+// y0 .. y0+h-1 at full width (background outside the region) and one record
+// per region pixel, row-major; *seconds is the wall time of the reference's
+// sweeps (the region filter excluded).  The accumulator is int64, falling
+// back to Int128 on the reference's OverflowError when allow_fallback
+// (*bits_used tells which; raycast_tests.cpp:440-442 equates the two).
+int rp_render_region(const rp_particle* ps, std::size_t n, const rp_camera* c,
+                     const rp_tf_point* tfp, std::size_t ntf, void* lutp, const rp_quanta* q,
+                     double step, const double* bg, int threads, int x0, int y0, int w, int h,
+                     int allow_fallback, double* rgb, rp_ray_record* rec, rp_rstats* st,
+                     double* seconds, int* bits_used, rp_error* err) {
+    return guarded(err, [&] {
+        const Camera cam = to_cam(c);
+        cam.validate();
+        const TransferFunction tf = to_tf(tfp, ntf);
+        tf.validate();
+        const Lut& lut = *static_cast<Lut*>(lutp);
+        const QuantaConfig qc = to_qc(q);
+        const int D = lut.D;
+        const int W = cam.width;
+        const Region reg = make_region(cam, x0, y0, w, h);
+        const int RW = reg.x1 - reg.x0;
+        const std::size_t nrow_px = static_cast<std::size_t>(reg.y1 - reg.y0) * W;
+        const std::size_t nreg = static_cast<std::size_t>(reg.y1 - reg.y0) * RW;
+        auto at = [&](std::uint64_t id) {
+            return static_cast<std::size_t>(id / W - reg.y0) * RW + (id % W - reg.x0);
+        };
+        const std::span<const Particle> all = to_span(ps, n);
+        std::vector<std::uint32_t> keep;
+        for (std::size_t i = 0; i < n; ++i)
+            if (may_reach(all[i], cam, lut.q, reg)) keep.push_back(static_cast<std::uint32_t>(i));
+        const double stp = step;
+        auto run = [&](auto tag) {
+            using Int = typename decltype(tag)::type;
+            const int nthreads = resolve_threads(threads);
+            const auto t0 = std::chrono::steady_clock::now();
+            // sweep 1 (raycast.hpp:427-446) over the particles that can reach the region
+            std::vector<std::vector<QuantizedKnot<Int>>> buffers(nthreads);
+            std::vector<std::vector<std::uint64_t>> hit_rays(nthreads);
+            const std::size_t chunk = (keep.size() + nthreads - 1) / nthreads;
+            parallel_for(buffers.size(), nthreads, [&](std::size_t b) {
+                const std::size_t lo = b * chunk, hi = std::min(lo + chunk, keep.size());
+                for (std::size_t k = lo; k < hi; ++k) {
+                    const std::size_t i = keep[k];
+                    auto hits = particle_ray_footprint(all[i], cam, lut.q);
+                    for (const auto& hit : hits) {
+                        if (!reg.contains(hit.ray.px, hit.ray.py)) continue;
+                        hit_rays[b].push_back(hit.ray.id);
+                        auto ks = quantize_particle<Int>(all[i], hit.ray.id, hit.t_chi, hit.lam, lut,
+                                                         qc, static_cast<std::int64_t>(i));
+                        buffers[b].insert(buffers[b].end(), ks.begin(), ks.end());
+                    }
+                }
+            });
+            std::vector<QuantizedKnot<Int>> knots;
+            for (auto& b : buffers) knots.insert(knots.end(), b.begin(), b.end());
+            buffers.clear();
+            sort_knots(knots);  // sweep 2
+            std::vector<std::size_t> starts;
+            for (std::size_t i = 0; i < knots.size(); ++i)
+                if (i == 0 || knots[i].ray != knots[i - 1].ray) starts.push_back(i);
+            starts.push_back(knots.size());
+            const std::size_t nrays = starts.size() - 1;
+            std::vector<Rgb> px(nrow_px, Rgb{bg[0], bg[1], bg[2]});
+            std::vector<std::vector<FieldPiece<Int>>> pieces(nrays);
+            std::vector<std::uint64_t> ops(nrays, 0);
+            std::vector<double> Tend(nrays, 1.0);
+            parallel_for(nrays, nthreads, [&](std::size_t r) {  // sweep 3
+                const std::span<const QuantizedKnot<Int>> stream(knots.data() + starts[r],
+                                                                 starts[r + 1] - starts[r]);
+                pieces[r] = accumulate(stream, D, &ops[r]);
+                const std::uint64_t id = stream[0].ray;
+                const Rgba cc = composite<Int>(pieces[r], qc, D, tf, stp, cam.near, cam.far);
+                Tend[r] = 1.0 - cc.a;
+                px[(id / W - reg.y0) * W + id % W] = {cc.r + (1.0 - cc.a) * bg[0],
+                                                      cc.g + (1.0 - cc.a) * bg[1],
+                                                      cc.b + (1.0 - cc.a) * bg[2]};
+            });
+            const auto t1 = std::chrono::steady_clock::now();
+            *seconds = std::chrono::duration<double>(t1 - t0).count();
+            for (std::size_t i = 0; i < nrow_px; ++i) {
+                rgb[3 * i + 0] = px[i].r;
+                rgb[3 * i + 1] = px[i].g;
+                rgb[3 * i + 2] = px[i].b;
+            }
+            std::memset(rec, 0, nreg * sizeof(rp_ray_record));
+            for (const auto& hr : hit_rays)
+                for (std::uint64_t id : hr) rec[at(id)].hits++;
+            rp_rstats s{};
+            s.particles = n;
+            s.knots = knots.size();
+            s.rays_touched = nrays;
+            s.step = stp;
+            for (std::size_t r = 0; r < nrays; ++r) {
+                rp_ray_record& o = rec[at(knots[starts[r]].ray)];
+                o.knots = static_cast<std::uint32_t>(starts[r + 1] - starts[r]);
+                o.pieces = static_cast<std::uint32_t>(pieces[r].size());
+                o.flags = 1u;
+                std::uint64_t cs = 0;
+                for (const auto& pc : pieces[r]) {
+                    std::int64_t a[max_degree + 1];
+                    for (int d = 0; d <= D; ++d) a[d] = static_cast<std::int64_t>(pc.a[d]);
+                    cs += piece_mix(static_cast<std::int64_t>(pc.t), a, D);
+                }
+                bool zero = true;
+                for (int d = 0; d <= D; ++d)
+                    if (pieces[r].back().a[d] != Int{}) zero = false;
+                if (!zero) {
+                    o.flags |= 2u;
+                    ++s.residual_failures;
+                }
+                if (!(Tend[r] > 1e-3)) o.flags |= 4u;
+                o.piece_checksum = cs;
+                s.int_ops += ops[r];
+            }
+            *st = s;
+        };
+        try {
+            *bits_used = 64;
+            run(std::type_identity<std::int64_t>{});
+        } catch (const OverflowError&) {
+            if (!allow_fallback) throw;
+            *bits_used = 128;
+            run(std::type_identity<Int128>{});
+        }
+    });
+}
+
+int rp_generate_scene(int config, std::size_t n, std::uint64_t seed, rp_particle* out, rp_error* err) {
+    return guarded(err, [&] {
+        if (sphray_scenes::default_count(config) == 0) throw ConfigError("unknown scene config");
+        if (n == 0) n = sphray_scenes::default_count(config);
+        sphray_scenes::generate(config, n, seed, reinterpret_cast<sphray_scenes::Record*>(out));
+    });
+}
+
+std::size_t rp_scene_default_count(int config) { return sphray_scenes::default_count(config); }
 
 // Reference loaders (io.hpp) for the bundled desk scene fixtures.
 std::int64_t rp_load_particles(const char* path, rp_particle* out, std::size_t cap,

@@ -138,7 +138,17 @@ class _RStats(C.Structure):
         ("step", C.c_double)] + [(n, C.c_uint64) for n in (
             "hits", "candidates", "window_retries", "max_window")] + [
         ("device_ms", C.c_double), ("bin_ms", C.c_double), ("render_ms", C.c_double),
-        ("launches", C.c_uint64)]
+        ("launches", C.c_uint64), ("terminated_rays", C.c_uint64)]
+
+
+class _RayRecord(C.Structure):
+    _fields_ = [("piece_checksum", C.c_uint64), ("knots", C.c_uint32), ("pieces", C.c_uint32),
+                ("hits", C.c_uint32), ("flags", C.c_uint32)]
+
+
+RAY_RECORD_DTYPE = np.dtype([("piece_checksum", "<u8"), ("knots", "<u4"), ("pieces", "<u4"),
+                             ("hits", "<u4"), ("flags", "<u4")])
+RAY_TOUCHED, RAY_RESIDUAL, RAY_TERMINATED = 1, 2, 4
 
 
 class _Error(C.Structure):
@@ -172,6 +182,11 @@ def load_library():
     L.sphray_comm_unique_id.argtypes = [C.c_char_p, P(_Error)]
     L.sphray_context_init_comm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p, P(_Error)]
     L.sphray_context_set_shard.argtypes = [C.c_void_p, C.c_int, C.c_int, P(_Error)]
+    L.sphray_context_set_region.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                            C.c_int32, P(_Error)]
+    L.sphray_scene_info.argtypes = [C.c_void_p, P(C.c_size_t), P(C.c_int32), P(C.c_int32), P(_Error)]
+    L.sphray_context_ray_records.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, P(C.c_size_t),
+                                             P(_Error)]
     L.sphray_render_scene.argtypes = [C.c_void_p, P(_Particle), C.c_size_t, P(_Camera),
                                       P(_TfPoint), C.c_size_t, P(_LutView), P(_Quanta),
                                       P(_DStats), P(_Options), P(C.c_double), P(_RStats),
@@ -212,7 +227,8 @@ def load_library():
     L.sphray_scene_default_count.argtypes = [C.c_int]
     L.sphray_scene_default_count.restype = C.c_size_t
     for name in ("sphray_context_create", "sphray_comm_unique_id", "sphray_context_init_comm",
-                 "sphray_context_set_shard",
+                 "sphray_context_set_shard", "sphray_context_set_region", "sphray_scene_info",
+                 "sphray_context_ray_records",
                  "sphray_render_scene", "sphray_scene_upload", "sphray_scene_render",
                  "sphray_scene_hits", "sphray_scene_pieces", "sphray_quantize_hits",
                  "sphray_compute_dataset_stats", "sphray_choose_quanta", "sphray_lut_parse",
@@ -359,6 +375,7 @@ class RenderStats:
     bin_ms: float = 0.0
     render_ms: float = 0.0
     launches: int = 0
+    terminated_rays: int = 0
 
     @classmethod
     def _from(cls, s: _RStats) -> "RenderStats":
@@ -564,6 +581,31 @@ class Context:
         _check(self._L.sphray_context_set_shard(self._h, rank, nranks, C.byref(err)), err)
         self._shard = (rank, nranks)
 
+    def set_region(self, x0: int = 0, y0: int = 0, w: int = 0, h: int = 0, record: bool = False):
+        """Trace only pixels [x0, x0+w) x [y0, y0+h) of later frames (the same rays
+        as the full frame; w or h == 0: full frames); render() then returns rows
+        y0 .. y0+h-1.  record: keep one per-ray record (knots, pieces, hits,
+        flags, piece checksum) per pixel of the region, row-major."""
+        err = _Error()
+        _check(self._L.sphray_context_set_region(self._h, int(x0), int(y0), int(w), int(h),
+                                                 int(bool(record)), C.byref(err)), err)
+        self._rows = (int(y0), int(h) if w > 0 else 0)
+
+    def scene_info(self) -> dict:
+        """The resident scene: particle count n and the LUT's K, D (sphray_scene_info)."""
+        n, K, D, err = C.c_size_t(), C.c_int32(), C.c_int32(), _Error()
+        _check(self._L.sphray_scene_info(self._h, C.byref(n), C.byref(K), C.byref(D), C.byref(err)), err)
+        return {"n": n.value, "K": K.value, "D": D.value}
+
+    def ray_records(self) -> np.ndarray:
+        """Per-ray records of the last frame (row-major over the band), RAY_RECORD_DTYPE."""
+        cnt, err = C.c_size_t(), _Error()
+        _check(self._L.sphray_context_ray_records(self._h, None, 0, C.byref(cnt), C.byref(err)), err)
+        out = np.zeros(cnt.value, RAY_RECORD_DTYPE)
+        _check(self._L.sphray_context_ray_records(self._h, out.ctypes.data_as(C.c_void_p), len(out),
+                                                  C.byref(cnt), C.byref(err)), err)
+        return out
+
     def upload(self, particles, lut: Lut):
         a = _particles(particles)
         err = _Error()
@@ -585,13 +627,15 @@ class Context:
             nt = _d.tile_grid(cam.width, cam.height)[2]
             shape = (_d.packed_tiles_per_rank(shard[1], nt) * _d.TILE * _d.TILE * 3,)
         else:
-            shape = (cam.height, cam.width, 3)
+            r0, nr = getattr(self, "_rows", (0, 0))
+            rows = cam.height if nr == 0 else max(0, min(r0 + nr, cam.height) - min(r0, cam.height))
+            shape = (rows, cam.width, 3)
         rgb = np.empty(shape, dtype=np.float64) if to_host else None
         _check(self._L.sphray_scene_render(
             self._h, C.byref(c), tfa, ntf, C.byref(q), C.byref(ds), C.byref(o),
             rgb.ctypes.data_as(C.POINTER(C.c_double)) if to_host else None, C.byref(rs),
             C.byref(err)), err)
-        img = Image(cam.width, cam.height, rgb) if to_host else None
+        img = Image(cam.width, shape[0] if shard[1] == 1 else cam.height, rgb) if to_host else None
         return img, RenderStats._from(rs)
 
     def stream_ptr(self) -> int:
@@ -624,7 +668,7 @@ class Context:
         nr, npc, err = C.c_size_t(), C.c_size_t(), _Error()
         _check(self._L.sphray_scene_pieces(self._h, C.byref(c), C.byref(q), None, None, None, None,
                                            0, 0, C.byref(nr), C.byref(npc), C.byref(err)), err)
-        D = self._lut.D
+        D = self.scene_info()["D"]  # the stride the library writes (the resident scene's degree)
         rays = np.zeros(nr.value, np.uint64)
         off = np.zeros(nr.value + 1, np.uint64)
         pt = np.zeros(npc.value, np.int64)
@@ -655,6 +699,8 @@ class Context:
         err = _Error()
         _check(self._L.sphray_scene_upload_file(self._h, os.fsencode(path), C.byref(lut.view),
                                                 C.byref(err)), err)
+        self._lut = lut
+        self._n = self.scene_info()["n"]
 
     def dataset_stats(self, clustering_factor: float = 16.0) -> DatasetStats:
         """dataset_stats (quantize.hpp:129-165) of the uploaded scene, on the GPU."""

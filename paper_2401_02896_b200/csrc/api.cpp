@@ -139,6 +139,30 @@ sphray_status sphray_scene_render(sphray_context* ctx, const sphray_camera* cam,
     });
 }
 
+sphray_status sphray_scene_info(sphray_context* ctx, size_t* n, int32_t* K, int32_t* D,
+                                sphray_error* err) {
+    return guarded(err, [&] {
+        Engine& e = engine(ctx);
+        if (!e.has_scene()) fail(SPHRAY_ERR_CONFIG, "no scene uploaded");
+        if (n) *n = e.scene_size();
+        if (K) *K = e.scene_K();
+        if (D) *D = e.scene_D();
+    });
+}
+
+sphray_status sphray_context_set_region(sphray_context* ctx, int32_t x0, int32_t y0, int32_t w,
+                                        int32_t h, int32_t record_rays, sphray_error* err) {
+    return guarded(err, [&] { engine(ctx).set_region(x0, y0, w, h, record_rays != 0); });
+}
+
+sphray_status sphray_context_ray_records(sphray_context* ctx, sphray_ray_record* out, size_t cap,
+                                         size_t* count, sphray_error* err) {
+    return guarded(err, [&] {
+        const size_t n = engine(ctx).ray_records(out, cap);
+        if (count) *count = n;
+    });
+}
+
 void* sphray_context_stream(sphray_context* ctx) {
     if (!ctx || !ctx->engine) return nullptr;
     return ctx->engine->stream();

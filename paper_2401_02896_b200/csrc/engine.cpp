@@ -175,77 +175,111 @@ void Engine::set_shard(int rank, int nranks) {
     nranks_ = nranks;
 }
 
+void Engine::set_region(int x0, int y0, int w, int h, bool record) {
+    if (x0 < 0 || y0 < 0 || w < 0 || h < 0) fail(SPHRAY_ERR_CONFIG, "set_region: negative coordinate or size");
+    if (w > 0 && h > 0 && nranks_ > 1) fail(SPHRAY_ERR_CONFIG, "set_region: regions need a single-rank context");
+    reg_x0_ = x0;
+    reg_y0_ = y0;
+    reg_w_ = w;
+    reg_h_ = h;
+    record_ = record;
+    n_records_ = 0;
+}
+
+size_t Engine::ray_records(sphray_ray_record* out, size_t cap) {
+    set_device();
+    if (out && cap) {
+        const size_t k = std::min(cap, n_records_);
+        CUDA_OK(cudaMemcpy(out, d_rec_.p, k * sizeof(sphray_ray_record), cudaMemcpyDeviceToHost));
+    }
+    return n_records_;
+}
+
 void Engine::upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_view& lutv) {
     set_device();
-    lut_ = make_lut(lutv);
+    // The new scene is built in locals and committed only when every
+    // allocation and copy succeeded; until then the context holds no scene
+    // (a failed upload never leaves n_ / lut_ describing smaller buffers).
+    has_scene_ = false;
+    LutHost lut = make_lut(lutv);
     if (n >= static_cast<size_t>(INT32_MAX)) fail(SPHRAY_ERR_CONFIG, "too many particles");
     if (n > 0 && !ps) fail(SPHRAY_ERR_CONFIG, "null particle pointer");
-    n_ = n;
-    const int D = lut_.D;
-    d_lut_.ensure(lut_.rows.size() * sizeof(double));
-    CUDA_OK(cudaMemcpyAsync(d_lut_.p, lut_.rows.data(), lut_.rows.size() * sizeof(double),
+    const int D = lut.D;
+    d_lut_.ensure(lut.rows.size() * sizeof(double));
+    CUDA_OK(cudaMemcpyAsync(d_lut_.p, lut.rows.data(), lut.rows.size() * sizeof(double),
                             cudaMemcpyHostToDevice, stream_));
-    has_scene_ = true;
-    scene_extent_ = 0.0;
-    if (n == 0) {
-        CUDA_OK(cudaStreamSynchronize(stream_));
-        return;
+    double extent = 0.0;
+    if (n > 0) {
+        // The raw particles go up on the aux stream from a helper thread (a
+        // pageable copy holds its calling thread) while this thread computes
+        // pow(h, d+3) with glibc (quantize.hpp:222, the one libm call per
+        // particle) and the bounding box for the Morton codes.  Every buffer
+        // is allocated before the thread starts, and the thread is joined on
+        // every path out of this scope.
+        d_raw_.ensure(n * sizeof(sphray_particle));
+        d_powh_raw_.ensure(n * D * sizeof(double));
+        h_powh_.ensure(n * D * sizeof(double));
+        d_codes_.ensure(n * 8);
+        d_codes2_.ensure(n * 8);
+        d_idx_.ensure(n * 4);
+        d_idx2_.ensure(n * 4);
+        d_pxyzh_.ensure(n * sizeof(double4));
+        d_mvr_.ensure(n * sizeof(double4));
+        d_powh_.ensure(n * D * sizeof(double));
+        d_orig_.ensure(n * sizeof(int32_t));
+        cudaError_t copy_rc = cudaSuccess;
+        double lo[3], hi[3];
+        {
+            std::thread copier([&] {
+                copy_rc = cudaSetDevice(device_);
+                if (copy_rc == cudaSuccess)
+                    copy_rc = cudaMemcpyAsync(d_raw_.p, ps, n * sizeof(sphray_particle),
+                                              cudaMemcpyHostToDevice, aux_);
+                if (copy_rc == cudaSuccess) copy_rc = cudaStreamSynchronize(aux_);
+            });
+            struct Joiner {
+                std::thread& t;
+                ~Joiner() {
+                    if (t.joinable()) t.join();
+                }
+            } joiner{copier};
+            particle_powers_bbox(ps, n, D, static_cast<double*>(h_powh_.p), lo, hi);
+        }
+        CUDA_OK(copy_rc);
+        {
+            double hmax = 0.0;
+            for (size_t i = 0; i < n; i += std::max<size_t>(1, n / 65536)) hmax = std::max(hmax, ps[i].h);
+            const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+            extent = std::sqrt(dx * dx + dy * dy + dz * dz);
+            if (!std::isfinite(extent)) extent = 1e300;
+            extent += 4.0 * hmax * lut.q;  // knots reach about q h beyond a centre
+        }
+        double inv[3];
+        for (int a = 0; a < 3; ++a) {
+            const double ext = hi[a] - lo[a];
+            inv[a] = (ext > 0.0 && std::isfinite(ext)) ? 2097151.0 / ext : 0.0;
+            if (!std::isfinite(lo[a])) lo[a] = 0.0;
+        }
+        launch_morton(d_raw_.as<sphray_particle>(), n, lo, inv, d_codes_.as<unsigned long long>(),
+                      d_idx_.as<uint32_t>(), stream_);
+        d_tmp_.ensure(radix_tmp_bytes(n));
+        const bool alt = sort_pairs_u64(d_codes_.as<unsigned long long>(), d_codes2_.as<unsigned long long>(),
+                                        d_idx_.as<uint32_t>(), d_idx2_.as<uint32_t>(), n, 63, d_tmp_.p, stream_);
+        const uint32_t* perm = alt ? d_idx2_.as<uint32_t>() : d_idx_.as<uint32_t>();
+        // the powers go up while the device sorts
+        CUDA_OK(cudaMemcpyAsync(d_powh_raw_.p, h_powh_.p, n * D * sizeof(double),
+                                cudaMemcpyHostToDevice, aux_));
+        CUDA_OK(cudaEventRecord(ev_aux_, aux_));
+        CUDA_OK(cudaStreamWaitEvent(stream_, ev_aux_, 0));
+        launch_scatter_scene(d_raw_.as<sphray_particle>(), d_powh_raw_.as<double>(), perm, n, D, d_pxyzh_.as<double4>(), d_mvr_.as<double4>(),
+                             d_powh_.as<double>(), d_orig_.as<int32_t>(), stream_);
     }
-    // The raw particles go up on the aux stream from a helper thread (a
-    // pageable copy holds its calling thread) while this thread computes
-    // pow(h, d+3) with glibc (quantize.hpp:222, the one libm call per
-    // particle) and the bounding box for the Morton codes.
-    d_raw_.ensure(n * sizeof(sphray_particle));
-    d_powh_raw_.ensure(n * D * sizeof(double));
-    cudaError_t copy_rc = cudaSuccess;
-    std::thread copier([&] {
-        copy_rc = cudaSetDevice(device_);
-        if (copy_rc == cudaSuccess)
-            copy_rc = cudaMemcpyAsync(d_raw_.p, ps, n * sizeof(sphray_particle), cudaMemcpyHostToDevice, aux_);
-        if (copy_rc == cudaSuccess) copy_rc = cudaStreamSynchronize(aux_);
-    });
-    h_powh_.ensure(n * D * sizeof(double));
-    double lo[3], hi[3];
-    particle_powers_bbox(ps, n, D, static_cast<double*>(h_powh_.p), lo, hi);
-    copier.join();
-    CUDA_OK(copy_rc);
-    {
-        double hmax = 0.0;
-        for (size_t i = 0; i < n; i += std::max<size_t>(1, n / 65536)) hmax = std::max(hmax, ps[i].h);
-        const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
-        scene_extent_ = std::sqrt(dx * dx + dy * dy + dz * dz);
-        if (!std::isfinite(scene_extent_)) scene_extent_ = 1e300;
-        scene_extent_ += 4.0 * hmax * lut_.q;  // knots reach about q h beyond a centre
-    }
-    double inv[3];
-    for (int a = 0; a < 3; ++a) {
-        const double ext = hi[a] - lo[a];
-        inv[a] = (ext > 0.0 && std::isfinite(ext)) ? 2097151.0 / ext : 0.0;
-        if (!std::isfinite(lo[a])) lo[a] = 0.0;
-    }
-    d_codes_.ensure(n * 8);
-    d_codes2_.ensure(n * 8);
-    d_idx_.ensure(n * 4);
-    d_idx2_.ensure(n * 4);
-    launch_morton(d_raw_.as<sphray_particle>(), n, lo, inv, d_codes_.as<unsigned long long>(),
-                  d_idx_.as<uint32_t>(), stream_);
-    const size_t sb = cub_sort_bytes(n, 63);
-    d_tmp_.ensure(sb);
-    cub_sort(d_codes_.as<unsigned long long>(), d_codes2_.as<unsigned long long>(),
-             d_idx_.as<uint32_t>(), d_idx2_.as<uint32_t>(), n, 63, d_tmp_.p, d_tmp_.bytes, stream_);
-    // the powers go up while the device sorts
-    CUDA_OK(cudaMemcpyAsync(d_powh_raw_.p, h_powh_.p, n * D * sizeof(double),
-                            cudaMemcpyHostToDevice, aux_));
-    CUDA_OK(cudaEventRecord(ev_aux_, aux_));
-    CUDA_OK(cudaStreamWaitEvent(stream_, ev_aux_, 0));
-    d_pxyzh_.ensure(n * sizeof(double4));
-    d_mvr_.ensure(n * sizeof(double4));
-    d_powh_.ensure(n * D * sizeof(double));
-    d_orig_.ensure(n * sizeof(int32_t));
-    launch_scatter_scene(d_raw_.as<sphray_particle>(), d_powh_raw_.as<double>(),
-                         d_idx2_.as<uint32_t>(), n, D, d_pxyzh_.as<double4>(), d_mvr_.as<double4>(),
-                         d_powh_.as<double>(), d_orig_.as<int32_t>(), stream_);
     CUDA_OK(cudaStreamSynchronize(stream_));
+    lut_ = std::move(lut);
+    n_ = n;
+    scene_extent_ = extent;
+    shape_key_[0] = -1;  // re-derive the render CTA shape for the new LUT
+    has_scene_ = true;
 }
 
 namespace {
@@ -581,8 +615,27 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     const size_t npix = static_cast<size_t>(W) * H;
     const int tiles_x = (W + kTile - 1) / kTile, tiles_y = (H + kTile - 1) / kTile;
     const uint64_t ntiles = static_cast<uint64_t>(tiles_x) * tiles_y;
-    const uint64_t owned = (ntiles + nranks_ - 1 - rank_) / nranks_;
+    uint64_t owned = (ntiles + nranks_ - 1 - rank_) / nranks_;
     const uint64_t owned_max = (ntiles + nranks_ - 1) / nranks_;
+    // pixel region (set_region): the same rays as the full frame, only
+    // px in [col_lo, col_hi), py in [row_lo, row_hi)
+    int row_lo = 0, row_hi = H, col_lo = 0, col_hi = W, tile_row0 = 0, tile_col0 = 0, tiles_wx = tiles_x;
+    if (reg_w_ > 0 && reg_h_ > 0) {
+        if (nranks_ > 1) fail(SPHRAY_ERR_CONFIG, "pixel regions need a single-rank context");
+        row_lo = std::min(reg_y0_, H);
+        row_hi = std::min(reg_y0_ + reg_h_, H);
+        col_lo = std::min(reg_x0_, W);
+        col_hi = std::min(reg_x0_ + reg_w_, W);
+        tile_row0 = row_lo >> kTileShift;
+        tile_col0 = col_lo >> kTileShift;
+        owned = 0;
+        tiles_wx = 0;
+        if (row_hi > row_lo && col_hi > col_lo) {
+            tiles_wx = ((col_hi - 1) >> kTileShift) - tile_col0 + 1;
+            owned = static_cast<uint64_t>(tiles_wx) * (((row_hi - 1) >> kTileShift) - tile_row0 + 1);
+        }
+    }
+    const size_t band_rays = static_cast<size_t>(row_hi - row_lo) * W;  // records / rows copied back
     const int n = static_cast<int>(n_);
     cudaStream_t s = stream_;
 
@@ -613,6 +666,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     d_stats_.ensure(kStatCount * 8);
     CUDA_OK(cudaMemsetAsync(d_stats_.p, 0, kStatCount * 8, s));
     CUDA_OK(cudaMemsetAsync(d_stats_.as<unsigned long long>() + kStatOverflowKey, 0xff, 8, s));
+    CUDA_OK(cudaMemsetAsync(d_stats_.as<unsigned long long>() + kStatAccumOverflowRay, 0xff, 8, s));
     d_work_.ensure(16);
     d_retry_count_.ensure(16);
     d_dump_count_.ensure(16);
@@ -620,14 +674,40 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
 
     CUDA_OK(cudaEventRecord(ev0_, s));
     uint64_t launches = 0;
-    // ---- binning: reference bbox -> (tile, front) keys -> radix sort
+    // ---- binning (the acceleration structure, hand-written sorts in sort.cu):
+    // reference bbox per particle -> depth order of the particles (stable
+    // radix sort of the front bounds) -> (tile, particle) entries emitted in
+    // depth order -> stable radix sort by tile, so each tile's candidate list
+    // is in front order.
     uint64_t entries = 0;
+    // rank-local failures are deferred until every rank has reached the
+    // collective below (a throw here would leave the other ranks hanging)
+    int defer_code = 0;
+    std::string defer_msg;
+    auto defer = [&](int code, std::string msg) {
+        if (!defer_code) {
+            defer_code = code;
+            defer_msg = std::move(msg);
+        }
+    };
+    d_tile_begin_.ensure(owned_max * 4);
+    d_tile_end_.ensure(owned_max * 4);
+    CUDA_OK(cudaMemsetAsync(d_tile_begin_.p, 0, owned_max * 4, s));
+    CUDA_OK(cudaMemsetAsync(d_tile_end_.p, 0, owned_max * 4, s));
     if (n > 0) {
-        d_bbox_.ensure(static_cast<size_t>(n) * sizeof(int4));
-        d_front_.ensure(static_cast<size_t>(n) * sizeof(float));
-        d_xy_.ensure(static_cast<size_t>(n) * 3 * D * sizeof(double));
-        d_counts_.ensure(static_cast<size_t>(n) * 4);
-        d_offsets_.ensure(static_cast<size_t>(n) * 4);
+        const size_t un = static_cast<size_t>(n);
+        d_bbox_.ensure(un * sizeof(int4));
+        d_front_.ensure(un * sizeof(float));
+        d_xy_.ensure(un * 3 * D * sizeof(double));
+        d_counts_.ensure(un * 4);
+        d_counts2_.ensure(un * 4);
+        d_offsets_.ensure(un * 4);
+        d_dkeys_.ensure(un * 4);
+        d_dkeys2_.ensure(un * 4);
+        d_order_.ensure(un * 4);
+        d_order2_.ensure(un * 4);
+        d_total_.ensure(8);
+        d_tmp_.ensure(std::max(radix_tmp_bytes(un), scan_tmp_bytes(un)));
         PrepParams pp{};
         pp.cam = C;
         pp.n = n;
@@ -647,45 +727,39 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         pp.rank = rank_;
         pp.nranks = nranks_;
         launch_prep(pp, s);
-        launches += 1 + 2;  // k_prep + CUB scan (init + scan)
-        const size_t scan_b = cub_scan_bytes(n);
-        d_tmp_.ensure(scan_b);
-        cub_scan(d_counts_.as<uint32_t>(), d_offsets_.as<uint32_t>(), n, d_tmp_.p, d_tmp_.bytes, s);
-        uint32_t tail[2];
-        CUDA_OK(cudaMemcpyAsync(&tail[0], d_offsets_.as<uint32_t>() + (n - 1), 4, cudaMemcpyDeviceToHost, s));
-        CUDA_OK(cudaMemcpyAsync(&tail[1], d_counts_.as<uint32_t>() + (n - 1), 4, cudaMemcpyDeviceToHost, s));
+        launch_depth_keys(d_front_.as<float>(), n, d_dkeys_.as<uint32_t>(), d_order_.as<uint32_t>(), s);
+        const bool o2 = sort_pairs_u32(d_dkeys_.as<uint32_t>(), d_dkeys2_.as<uint32_t>(), d_order_.as<uint32_t>(),
+                                       d_order2_.as<uint32_t>(), un, 32, d_tmp_.p, s);
+        const uint32_t* order = o2 ? d_order2_.as<uint32_t>() : d_order_.as<uint32_t>();
+        CUDA_OK(cudaMemsetAsync(d_total_.p, 0, 8, s));
+        launch_gather_counts(d_counts_.as<uint32_t>(), order, n, d_counts2_.as<uint32_t>(),
+                             d_total_.as<unsigned long long>(), s);
+        scan_u32(d_counts2_.as<uint32_t>(), d_offsets_.as<uint32_t>(), un, d_tmp_.p, nullptr, s);
+        unsigned long long total = 0;
+        CUDA_OK(cudaMemcpyAsync(&total, d_total_.p, 8, cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaStreamSynchronize(s));
-        trace.mark("prep+scan");
-        entries = static_cast<uint64_t>(tail[0]) + tail[1];
-        if (entries >= 0xffffffffull)
-            fail(SPHRAY_ERR_CAPACITY, "more than 2^32 (tile, particle) entries; shard over more ranks");
-        d_tile_begin_.ensure(owned_max * 4);
-        d_tile_end_.ensure(owned_max * 4);
-        CUDA_OK(cudaMemsetAsync(d_tile_begin_.p, 0, owned_max * 4, s));
-        CUDA_OK(cudaMemsetAsync(d_tile_end_.p, 0, owned_max * 4, s));
+        launches += 2 + 3 * radix_passes(32) + 1 + 3;  // prep, depth keys, sort, gather, scan
+        trace.mark("prep+depth+scan");
+        if (total >= 0xffffffffull) {
+            defer(SPHRAY_ERR_CAPACITY, "more than 2^32 (tile, particle) entries; shard over more ranks");
+        } else {
+            entries = total;
+        }
         if (entries > 0) {
-            d_keys_.ensure(entries * 8);
-            d_keys2_.ensure(entries * 8);
+            d_keys_.ensure(entries * 4);
+            d_keys2_.ensure(entries * 4);
             d_vals_.ensure(entries * 4);
             d_vals2_.ensure(entries * 4);
-            launch_emit(pp, d_offsets_.as<uint32_t>(), d_keys_.as<unsigned long long>(),
-                        d_vals_.as<uint32_t>(), s);
-            const int end_bit = 32 + bits_for(owned_max);
-            const size_t sb = cub_sort_bytes(entries, end_bit);
-            d_tmp_.ensure(sb);
-            cub_sort(d_keys_.as<unsigned long long>(), d_keys2_.as<unsigned long long>(),
-                     d_vals_.as<uint32_t>(), d_vals2_.as<uint32_t>(), entries, end_bit, d_tmp_.p,
-                     d_tmp_.bytes, s);
-            launch_tile_ranges(d_keys2_.as<unsigned long long>(), entries,
+            d_tmp_.ensure(radix_tmp_bytes(entries));
+            launch_emit(pp, order, d_offsets_.as<uint32_t>(), d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(), s);
+            const int end_bit = bits_for(owned_max);
+            const bool k2 = sort_pairs_u32(d_keys_.as<uint32_t>(), d_keys2_.as<uint32_t>(), d_vals_.as<uint32_t>(),
+                                           d_vals2_.as<uint32_t>(), entries, end_bit, d_tmp_.p, s);
+            cand_ = k2 ? d_vals2_.as<uint32_t>() : d_vals_.as<uint32_t>();
+            launch_tile_ranges(k2 ? d_keys2_.as<uint32_t>() : d_keys_.as<uint32_t>(), entries,
                                d_tile_begin_.as<uint32_t>(), d_tile_end_.as<uint32_t>(), s);
-            // k_emit + onesweep radix sort (histogram, exclusive sum, one pass per 8 bits) + ranges
-            launches += 1 + 2 + (end_bit + 7) / 8 + 1;
+            launches += 1 + 3 * radix_passes(end_bit) + 1;  // emit, sort, ranges
         }
-    } else {
-        d_tile_begin_.ensure(owned_max * 4);
-        d_tile_end_.ensure(owned_max * 4);
-        CUDA_OK(cudaMemsetAsync(d_tile_begin_.p, 0, owned_max * 4, s));
-        CUDA_OK(cudaMemsetAsync(d_tile_end_.p, 0, owned_max * 4, s));
     }
 
     // ---- output buffers
@@ -718,7 +792,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     P.bbox = d_bbox_.as<int4>();
     P.front = d_front_.as<float>();
     P.orig = d_orig_.as<int32_t>();
-    P.cand = d_vals2_.as<uint32_t>();
+    P.cand = cand_;
     P.tile_begin = d_tile_begin_.as<uint32_t>();
     P.tile_end = d_tile_end_.as<uint32_t>();
     P.tiles_x = tiles_x;
@@ -740,6 +814,21 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     P.rgb = target;
     P.packed = packed;
     P.stats = d_stats_.as<unsigned long long>();
+    P.tile_row0 = tile_row0;
+    P.tile_col0 = tile_col0;
+    P.tiles_wx = tiles_wx;
+    P.row_lo = row_lo;
+    P.row_hi = row_hi;
+    P.col_lo = col_lo;
+    P.col_hi = col_hi;
+    n_records_ = 0;
+    if (record_) {
+        const size_t nrec = static_cast<size_t>(row_hi - row_lo) * (col_hi - col_lo);
+        d_rec_.ensure(std::max<size_t>(nrec, 1) * sizeof(sphray_ray_record));
+        CUDA_OK(cudaMemsetAsync(d_rec_.p, 0, nrec * sizeof(sphray_ray_record), s));
+        P.ray_rec = d_rec_.as<sphray_ray_record>();
+        n_records_ = nrec;
+    }
     P.dump_count = d_dump_count_.as<unsigned long long>();
     d_retry_.ensure(npix * 4);
     d_retry2_.ensure(npix * 4);
@@ -849,7 +938,14 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
                       " ctas/sm=" + std::to_string(bps);
     CUDA_OK(cudaMemsetAsync(d_work_.p, 0, 8, s));
     CUDA_OK(cudaMemsetAsync(d_retry_count_.p, 0, 8, s));
+    if (reg_w_ > 0 && reg_h_ > 0 && band_rays > 0) {
+        // region frames: the rows handed back show the background outside the region
+        launch_fill_bg(d_image_.as<double>() + static_cast<size_t>(row_lo) * W * 3, band_rays,
+                       opts.background, s);
+        ++launches;
+    }
     CUDA_OK(cudaEventRecord(evr0_, s));
+    if (defer_code) P.total_work = 0;  // this rank failed: only join the collectives
     if (P.total_work > 0) {
         launch_render(P, D, m, sm_count_ * bps, warps, s);
         ++launches;
@@ -863,13 +959,18 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     trace.mark("render");
     // diagnostics (ncu captures of the main launch only): skip the retry pass
     if (std::getenv("SPHRAY_PROFILE_NO_RETRY")) retry = 0;
-    if (retry > 0 && dumps)
-        fail(SPHRAY_ERR_CAPACITY, std::to_string(retry) + " rays exceed the widest knot window (" +
-                                      std::to_string(cap) + " knots)");
+    if (retry > 0 && dumps) {
+        defer(SPHRAY_ERR_CAPACITY, std::to_string(retry) + " rays exceed the widest knot window (" +
+                                       std::to_string(cap) + " knots)");
+        retry = 0;
+    }
+    int cap2 = 65535;
+    while (cap2 > cap && warp_smem_bytes(D, cap2, m) + tfb > kSmemLimit) cap2 = cap2 * 15 / 16;
+    if (retry > 0 && cap2 <= cap) {
+        defer(SPHRAY_ERR_CAPACITY, "knot window cannot grow");
+        retry = 0;
+    }
     if (retry > 0) {
-        int cap2 = 65535;
-        while (cap2 > cap && warp_smem_bytes(D, cap2, m) + tfb > kSmemLimit) cap2 = cap2 * 15 / 16;
-        if (cap2 <= cap) fail(SPHRAY_ERR_CAPACITY, "knot window cannot grow");
         FrameParams P2 = P;
         P2.cap = cap2;
         P2.warp_bytes = static_cast<int>(warp_smem_bytes(D, cap2, m));
@@ -888,8 +989,8 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
                                 cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaStreamSynchronize(s));
         if (retry2 > 0)
-            fail(SPHRAY_ERR_CAPACITY, std::to_string(retry2) + " rays exceed the widest knot window (" +
-                                          std::to_string(cap2) + " knots)");
+            defer(SPHRAY_ERR_CAPACITY, std::to_string(retry2) + " rays exceed the widest knot window (" +
+                                           std::to_string(cap2) + " knots)");
     }
     CUDA_OK(cudaEventRecord(evr1_, s));
     // skipped_particles: counted once (rank 0), the particle set is replicated
@@ -899,10 +1000,25 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         ++launches;
     }
 
-    // ---- gather finished tiles over NCCL (image-tile sharding)
+    // ---- agree on rank-local failures, then gather finished tiles over NCCL
     unsigned long long st[kStatCount];
     if (packed && comm_) {
         auto& a = nccl();
+        d_status_.ensure(8 * (nranks_ + 1));
+        const long long mine = defer_code;
+        CUDA_OK(cudaMemcpyAsync(d_status_.p, &mine, 8, cudaMemcpyHostToDevice, s));
+        nccl_ok(a.AllGather(d_status_.p, d_status_.as<long long>() + 1, 1, ncclInt64,
+                            static_cast<ncclComm_t>(comm_), s),
+                "ncclAllGather(status)");
+        std::vector<long long> codes(nranks_);
+        CUDA_OK(cudaMemcpyAsync(codes.data(), d_status_.as<long long>() + 1, 8 * nranks_,
+                                cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        for (int r = 0; r < nranks_; ++r)
+            if (codes[r])
+                fail(static_cast<sphray_status>(codes[r]),
+                     r == rank_ ? defer_msg : "rank " + std::to_string(r) + " failed (status " +
+                                                  std::to_string(codes[r]) + ")");
         const size_t per_rank = owned_max * kTileRays * 3;
         d_gather_.ensure(per_rank * nranks_ * sizeof(double));
         nccl_ok(a.AllGather(d_packed_.p, d_gather_.p, per_rank, ncclDouble,
@@ -917,11 +1033,12 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         CUDA_OK(cudaMemcpyAsync(all.data(), d_stats_all_.p, all.size() * 8, cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaEventRecord(ev1_, s));
         CUDA_OK(cudaStreamSynchronize(s));
-        for (int k = 0; k < kStatCount; ++k) st[k] = (k == kStatOverflowKey) ? ~0ull : 0ull;
+        for (int k = 0; k < kStatCount; ++k)
+            st[k] = (k == kStatOverflowKey || k == kStatAccumOverflowRay) ? ~0ull : 0ull;
         for (int r = 0; r < nranks_; ++r)
             for (int k = 0; k < kStatCount; ++k) {
                 const unsigned long long v = all[r * kStatCount + k];
-                if (k == kStatOverflowKey)
+                if (k == kStatOverflowKey || k == kStatAccumOverflowRay)
                     st[k] = std::min(st[k], v);
                 else if (k == kStatMaxPending)
                     st[k] = std::max(st[k], v);
@@ -929,6 +1046,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
                     st[k] += v;
             }
     } else {
+        if (defer_code) fail(static_cast<sphray_status>(defer_code), defer_msg);
         CUDA_OK(cudaMemcpyAsync(st, d_stats_.p, sizeof(st), cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaEventRecord(ev1_, s));
         CUDA_OK(cudaStreamSynchronize(s));
@@ -940,7 +1058,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
                                       "resid<192", "resid<256", "resid<320", "resid<384", "resid>=384",
                                       "bits<=8", "bits<=10", "bits<=12", "bits<=14", "bits<=16",
                                       "bits>16"};
-        for (int k = kStatFirstK; k < kStatCount; ++k)
+        for (int k = kStatFirstK; k < kStatBits0 + 6; ++k)
             trace.line += std::string(" ") + names[k - kStatFirstK] + "=" + std::to_string(st[k]);
     }
     float ms = 0.0f, ms_bin = 0.0f, ms_render = 0.0f;
@@ -957,6 +1075,15 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
                  std::to_string(ray) + ")",
              pidx, ray);
     }
+    if (st[kStatAccumOverflowRay] != ~0ull) {
+        // accumulate's OverflowError names the ray (raycast.hpp:285-289); the
+        // GPU raises it only for a genuine overflow of a merged coefficient
+        // (the reference's int64 path also throws on spurious Delta t^D
+        // intermediates, which the exact wrapped merge does not need)
+        const uint64_t ray = st[kStatAccumOverflowRay];
+        fail(SPHRAY_ERR_OVERFLOW,
+             "accumulate: integer overflow (ray " + std::to_string(ray) + ")", -1, ray);
+    }
     if (st[kStatRays] > 0 && !(step > 0.0)) fail(SPHRAY_ERR_CONFIG, "composite: step must be positive");
 
     if (rgb_host) {
@@ -964,7 +1091,8 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
             CUDA_OK(cudaMemcpyAsync(rgb_host, d_packed_.p, owned_max * kTileRays * 3 * sizeof(double),
                                     cudaMemcpyDeviceToHost, s));
         else
-            CUDA_OK(cudaMemcpyAsync(rgb_host, d_image_.p, npix * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+            CUDA_OK(cudaMemcpyAsync(rgb_host, d_image_.as<double>() + static_cast<size_t>(row_lo) * W * 3,
+                                    band_rays * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaStreamSynchronize(s));
     }
     if (dumps) {
@@ -1010,6 +1138,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         o.bin_ms = ms_bin;
         o.render_ms = ms_render;
         o.launches = launches + (packed && comm_ ? 3 : 0);
+        o.terminated_rays = st[kStatTerminated];
         *out = o;
     }
 }

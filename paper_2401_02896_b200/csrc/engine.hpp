@@ -54,6 +54,10 @@ class Engine {
 
     void init_comm(int rank, int nranks, const uint8_t id[128]);
     void set_shard(int rank, int nranks);
+    // pixel region of subsequent renders (w or h == 0: full frames) and
+    // per-ray records (sphray_context_set_region)
+    void set_region(int x0, int y0, int w, int h, bool record);
+    size_t ray_records(sphray_ray_record* out, size_t cap);
     void upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_view& lut);
     // dataset_stats (quantize.hpp:129-165) of the uploaded scene, computed on the GPU
     sphray_dataset_stats scene_dataset_stats(double clustering_factor);
@@ -71,6 +75,9 @@ class Engine {
     const double* device_image() const { return d_image_.as<double>(); }
     void* stream() const { return stream_; }
     bool has_scene() const { return has_scene_; }
+    size_t scene_size() const { return n_; }
+    int scene_K() const { return lut_.K; }
+    int scene_D() const { return lut_.D; }
     int rank() const { return rank_; }
     int nranks() const { return nranks_; }
 
@@ -85,6 +92,11 @@ class Engine {
     // communicator (tile gather)
     int rank_ = 0, nranks_ = 1;
     void* comm_ = nullptr;
+    // row band + per-ray records
+    int reg_x0_ = 0, reg_y0_ = 0, reg_w_ = 0, reg_h_ = 0;
+    bool record_ = false;
+    size_t n_records_ = 0;
+    DevBuf d_rec_;
     // scene
     bool has_scene_ = false;
     size_t n_ = 0;
@@ -93,7 +105,9 @@ class Engine {
     DevBuf d_raw_, d_powh_raw_, d_codes_, d_codes2_, d_idx_, d_idx2_, d_tmp_;
     DevBuf d_pxyzh_, d_mvr_, d_powh_, d_orig_, d_lut_;
     // frame
-    DevBuf d_bbox_, d_front_, d_xy_, d_counts_, d_offsets_, d_keys_, d_keys2_, d_vals_, d_vals2_;
+    DevBuf d_bbox_, d_front_, d_xy_, d_counts_, d_counts2_, d_offsets_, d_keys_, d_keys2_, d_vals_, d_vals2_;
+    DevBuf d_dkeys_, d_dkeys2_, d_order_, d_order2_, d_total_, d_status_;
+    const uint32_t* cand_ = nullptr;  // sorted candidate list of the current frame
     DevBuf d_tile_begin_, d_tile_end_, d_tf_, d_powtau_, d_image_, d_packed_, d_gather_;
     DevBuf d_stats_, d_work_, d_retry_, d_retry2_, d_retry_count_;
     DevBuf d_dump_count_, d_dump_hr_, d_dump_hp_, d_dump_hl_, d_dump_ht_, d_dump_pr_, d_dump_pt_,

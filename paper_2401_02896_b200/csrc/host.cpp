@@ -1,5 +1,6 @@
 // host.cpp -- host-side pieces of the path (see host.hpp).
 #include "host.hpp"
+#include "sphray_scenes.hpp"
 
 #include <algorithm>
 #include <array>
@@ -423,96 +424,15 @@ void particle_powers_bbox(const sphray_particle* ps, size_t n, int D, double* ou
 }
 
 // ---------------------------------------------------------------------------
-// Synthetic scenes.
-size_t scene_default_count(int config) {
-    switch (config) {
-        case 1: return 100000;
-        case 2: return 1000000;
-        case 3: return 16777216;
-        case 4: return 4194304;
-        case 5: return 100000000;
-    }
-    return 0;
-}
-
-namespace {
-void blob(size_t n, uint64_t seed, double h, sphray_particle* out) {
-    std::mt19937_64 rng(seed);
-    std::normal_distribution<double> nd(0.0, 1.0);
-    const double mass = 1.0 / static_cast<double>(n);
-    for (size_t i = 0; i < n; ++i) {
-        const double x = nd(rng), y = nd(rng), z = nd(rng);
-        const double rho = std::exp(-(x * x + y * y + z * z) / 2.0) + 0.05;
-        out[i] = {x, y, z, mass, rho, h, rho};
-    }
-}
-
-// 256 Plummer halos + 10 % uniform background in [-3,3]^3; h from the
-// analytic mixture density: h = 1.2 (m / rho_model)^(1/3).
-void clustered(size_t n, uint64_t seed, sphray_particle* out) {
-    constexpr int kHalos = 256;
-    std::mt19937_64 rng(seed);
-    std::uniform_real_distribution<double> U(0.0, 1.0);
-    std::normal_distribution<double> nd(0.0, 1.0);
-    double cx[kHalos], cy[kHalos], cz[kHalos], a[kHalos], w[kHalos];
-    double wsum = 0.0;
-    for (int i = 0; i < kHalos; ++i) {
-        do {
-            cx[i] = 0.9 * nd(rng);
-            cy[i] = 0.9 * nd(rng);
-            cz[i] = 0.9 * nd(rng);
-        } while (std::fabs(cx[i]) > 2.5 || std::fabs(cy[i]) > 2.5 || std::fabs(cz[i]) > 2.5);
-        a[i] = std::exp(std::log(0.02) + (std::log(0.3) - std::log(0.02)) * U(rng));
-        w[i] = std::min(100.0, std::pow(1.0 - U(rng), -1.0 / 1.5));  // Pareto alpha = 1.5
-        wsum += w[i];
-    }
-    for (int i = 0; i < kHalos; ++i) w[i] = 0.9 * w[i] / wsum;  // mass fractions
-    const double mass = 1.0 / static_cast<double>(n);
-    size_t k = 0;
-    for (int i = 0; i < kHalos && k < n; ++i) {
-        const size_t cnt = std::min(n - k, static_cast<size_t>(w[i] * static_cast<double>(n)));
-        for (size_t j = 0; j < cnt; ++j, ++k) {
-            double r;
-            do {
-                const double u = std::max(U(rng), 1e-300);
-                r = a[i] / std::sqrt(std::pow(u, -2.0 / 3.0) - 1.0);
-            } while (!(r < 15.0 * a[i]));
-            const double ct = 2.0 * U(rng) - 1.0, ph = 2.0 * std::numbers::pi * U(rng);
-            const double st = std::sqrt(std::max(0.0, 1.0 - ct * ct));
-            out[k] = {cx[i] + r * st * std::cos(ph), cy[i] + r * st * std::sin(ph), cz[i] + r * ct,
-                      mass, 0.0, 0.0, 0.0};
-        }
-    }
-    for (; k < n; ++k)
-        out[k] = {-3.0 + 6.0 * U(rng), -3.0 + 6.0 * U(rng), -3.0 + 6.0 * U(rng), mass, 0.0, 0.0, 0.0};
-    double norm[kHalos];
-    for (int i = 0; i < kHalos; ++i) norm[i] = w[i] * 3.0 / (4.0 * std::numbers::pi * a[i] * a[i] * a[i]);
-    const double bg = 0.1 / 216.0;
-    parallel_chunks(n, [&](size_t lo, size_t hi) {
-        for (size_t p = lo; p < hi; ++p) {
-            double rho = bg;
-            for (int i = 0; i < kHalos; ++i) {
-                const double dx = out[p].x - cx[i], dy = out[p].y - cy[i], dz = out[p].z - cz[i];
-                const double s = 1.0 + (dx * dx + dy * dy + dz * dz) / (a[i] * a[i]);
-                rho += norm[i] / (s * s * std::sqrt(s));
-            }
-            out[p].density = rho;
-            out[p].value = rho;
-            out[p].h = 1.2 * std::cbrt(mass / rho);
-        }
-    });
-}
-}  // namespace
+// Synthetic scenes: include/sphray_scenes.hpp, shared with the
+// reference-side harness so both arms draw byte-identical particles.
+size_t scene_default_count(int config) { return sphray_scenes::default_count(config); }
 
 void generate_scene(int config, size_t n, uint64_t seed, sphray_particle* out) {
-    switch (config) {
-        case 1: blob(n, seed, n == 100000 ? 0.062 : 0.062 * std::cbrt(1e5 / n), out); return;
-        case 2: blob(n, seed, n == 1000000 ? 0.029 : 0.062 * std::cbrt(1e5 / n), out); return;
-        case 4: blob(n, seed, 0.062 * std::cbrt(1e5 / n), out); return;
-        case 3:
-        case 5: clustered(n, seed, out); return;
-    }
-    fail(SPHRAY_ERR_CONFIG, "unknown scene config " + std::to_string(config));
+    static_assert(sizeof(sphray_scenes::Record) == sizeof(sphray_particle), "record layout");
+    if (sphray_scenes::default_count(config) == 0)
+        fail(SPHRAY_ERR_CONFIG, "unknown scene config " + std::to_string(config));
+    sphray_scenes::generate(config, n, seed, reinterpret_cast<sphray_scenes::Record*>(out));
 }
 
 }  // namespace sphray_b200

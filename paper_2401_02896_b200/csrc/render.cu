@@ -18,8 +18,6 @@
 //   render_scene            raycast.hpp:414-497   -> k_render_rays + engine.cpp
 #include <cuda_runtime.h>
 
-#include <cub/cub.cuh>
-
 #include <cstring>
 
 #include "device_math.cuh"
@@ -71,34 +69,55 @@ __device__ __forceinline__ uint32_t orderable(float f) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-__global__ void k_emit(const PrepParams p, const uint32_t* offsets, unsigned long long* keys,
-                       uint32_t* vals) {
+__global__ void k_depth_keys(const float* front, int n, uint32_t* keys, uint32_t* vals) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= p.n) return;
+    if (i >= n) return;
+    keys[i] = orderable(front[i]);
+    vals[i] = static_cast<uint32_t>(i);
+}
+
+// counts in depth order, and their exact 64-bit total (the entry count)
+__global__ void k_gather_counts(const uint32_t* counts, const uint32_t* order, int n, uint32_t* out,
+                                unsigned long long* total) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long c = 0;
+    if (j < n) {
+        c = counts[order[j]];
+        out[j] = static_cast<uint32_t>(c);
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(total, c);
+}
+
+// Entries of the particle at depth rank j, at offsets[j]: the entry array is
+// in depth order, so a stable sort by tile leaves every tile's candidates
+// sorted by their front bound (what the render kernel's flush bound needs).
+__global__ void k_emit(const PrepParams p, const uint32_t* order, const uint32_t* offsets, uint32_t* keys,
+                       uint32_t* vals) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= p.n) return;
+    const uint32_t i = order[j];
     const int4 b = p.bbox[i];
     if (!(b.x <= b.y && b.z <= b.w)) return;
-    const uint32_t fk = orderable(p.front[i]);
-    uint32_t o = offsets[i];
+    uint32_t o = offsets[j];
     const int tx0 = b.x >> kTileShift, tx1 = b.y >> kTileShift;
     const int ty0 = b.z >> kTileShift, ty1 = b.w >> kTileShift;
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
             const uint32_t tile = static_cast<uint32_t>(ty * p.tiles_x + tx);
             if (p.nranks > 1 && static_cast<int>(tile % p.nranks) != p.rank) continue;
-            const uint32_t local = p.nranks > 1 ? tile / p.nranks : tile;
-            keys[o] = (static_cast<unsigned long long>(local) << 32) | fk;
-            vals[o] = static_cast<uint32_t>(i);
+            keys[o] = p.nranks > 1 ? tile / p.nranks : tile;
+            vals[o] = i;
             ++o;
         }
 }
 
-__global__ void k_tile_ranges(const unsigned long long* keys, size_t m, uint32_t* begin,
-                              uint32_t* end) {
+__global__ void k_tile_ranges(const uint32_t* keys, size_t m, uint32_t* begin, uint32_t* end) {
     const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;
-    const uint32_t t = static_cast<uint32_t>(keys[i] >> 32);
-    if (i == 0 || static_cast<uint32_t>(keys[i - 1] >> 32) != t) begin[t] = static_cast<uint32_t>(i);
-    if (i == m - 1 || static_cast<uint32_t>(keys[i + 1] >> 32) != t) end[t] = static_cast<uint32_t>(i + 1);
+    const uint32_t t = keys[i];
+    if (i == 0 || keys[i - 1] != t) begin[t] = static_cast<uint32_t>(i);
+    if (i == m - 1 || keys[i + 1] != t) end[t] = static_cast<uint32_t>(i + 1);
 }
 
 // skipped_particles (raycast.hpp:437-438, 452): particles with an empty footprint.
@@ -189,8 +208,16 @@ __global__ void k_scatter_scene(const sphray_particle* ps, const double* powh_in
 // dataset_stats (quantize.hpp:129-165) on the resident scene: the four
 // property columns for the medians, phi_max = max |(m v) / (((rho h) h) h)|
 // in the reference's operation order, and the positivity check of h, rho.
-__global__ void k_stats_columns(const double4* pxyzh, const double4* mvr, size_t n, double* mass,
-                                double* density, double* h, double* value,
+// dataset_stats columns as orderable u64 keys (the IEEE bit pattern with the
+// sign flipped / all bits flipped for negatives sorts like the doubles; -0.0
+// and +0.0 compare equal in std::sort and both give the same median value).
+__device__ __forceinline__ unsigned long long orderable_f64(double v) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(v));
+    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+__global__ void k_stats_columns(const double4* pxyzh, const double4* mvr, size_t n, unsigned long long* mass,
+                                unsigned long long* density, unsigned long long* h, unsigned long long* value,
                                 unsigned long long* phi_bits, unsigned int* bad) {
     const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     unsigned long long best = 0ull;
@@ -198,10 +225,10 @@ __global__ void k_stats_columns(const double4* pxyzh, const double4* mvr, size_t
     if (i < n) {
         const double4 p = pxyzh[i];
         const double4 q = mvr[i];
-        mass[i] = q.x;
-        value[i] = q.y;
-        density[i] = q.z;
-        h[i] = p.w;
+        mass[i] = orderable_f64(q.x);
+        value[i] = orderable_f64(q.y);
+        density[i] = orderable_f64(q.z);
+        h[i] = orderable_f64(p.w);
         b = !(p.w > 0.0) || !(q.z > 0.0);
         // p.mass * p.value / (p.density * p.h * p.h * p.h)   (host.cpp / quantize.hpp:141)
         const double num = __dmul_rn(q.x, q.y);
@@ -308,15 +335,27 @@ void launch_prep(const PrepParams& p, cudaStream_t s) {
     SPHRAY_CUDA_OK(cudaGetLastError());
 }
 
-void launch_emit(const PrepParams& p, const uint32_t* offsets, unsigned long long* keys,
-                 uint32_t* vals, cudaStream_t s) {
-    if (p.n == 0) return;
-    k_emit<<<grid_for(p.n, 256), 256, 0, s>>>(p, offsets, keys, vals);
+void launch_depth_keys(const float* front, int n, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+    if (n == 0) return;
+    k_depth_keys<<<grid_for(n, 256), 256, 0, s>>>(front, n, keys, vals);
     SPHRAY_CUDA_OK(cudaGetLastError());
 }
 
-void launch_tile_ranges(const unsigned long long* keys, size_t m, uint32_t* begin, uint32_t* end,
-                        cudaStream_t s) {
+void launch_gather_counts(const uint32_t* counts, const uint32_t* order, int n, uint32_t* out,
+                          unsigned long long* total, cudaStream_t s) {
+    if (n == 0) return;
+    k_gather_counts<<<grid_for(n, 256), 256, 0, s>>>(counts, order, n, out, total);
+    SPHRAY_CUDA_OK(cudaGetLastError());
+}
+
+void launch_emit(const PrepParams& p, const uint32_t* order, const uint32_t* offsets, uint32_t* keys,
+                 uint32_t* vals, cudaStream_t s) {
+    if (p.n == 0) return;
+    k_emit<<<grid_for(p.n, 256), 256, 0, s>>>(p, order, offsets, keys, vals);
+    SPHRAY_CUDA_OK(cudaGetLastError());
+}
+
+void launch_tile_ranges(const uint32_t* keys, size_t m, uint32_t* begin, uint32_t* end, cudaStream_t s) {
     if (m == 0) return;
     k_tile_ranges<<<grid_for(m, 256), 256, 0, s>>>(keys, m, begin, end);
     SPHRAY_CUDA_OK(cudaGetLastError());
@@ -370,35 +409,6 @@ void launch_quantize_hits(const QuantParams& Q, int D, const sphray_particle* ps
     });
 }
 
-size_t cub_scan_bytes(size_t n) {
-    size_t bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<const uint32_t*>(nullptr),
-                                  static_cast<uint32_t*>(nullptr), static_cast<int64_t>(n));
-    return bytes;
-}
-
-void cub_scan(const uint32_t* in, uint32_t* out, size_t n, void* tmp, size_t bytes, cudaStream_t s) {
-    if (n == 0) return;
-    SPHRAY_CUDA_OK(cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, static_cast<int64_t>(n), s));
-}
-
-size_t cub_sort_bytes(size_t n, int end_bit) {
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const unsigned long long*>(nullptr),
-                                    static_cast<unsigned long long*>(nullptr),
-                                    static_cast<const uint32_t*>(nullptr),
-                                    static_cast<uint32_t*>(nullptr), static_cast<int64_t>(n), 0,
-                                    end_bit);
-    return bytes;
-}
-
-void cub_sort(const unsigned long long* kin, unsigned long long* kout, const uint32_t* vin,
-              uint32_t* vout, size_t n, int end_bit, void* tmp, size_t bytes, cudaStream_t s) {
-    if (n == 0) return;
-    SPHRAY_CUDA_OK(cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout,
-                                                   static_cast<int64_t>(n), 0, end_bit, s));
-}
-
 namespace {
 struct Scratch {  // RAII device scratch for the one-off statistics pass
     void* p = nullptr;
@@ -413,32 +423,31 @@ struct Scratch {  // RAII device scratch for the one-off statistics pass
 
 void device_dataset_stats(const double4* pxyzh, const double4* mvr, size_t n, cudaStream_t s,
                           double med[4], double* phi_max, bool* bad) {
-    Scratch cols(n * 4 * sizeof(double)), sorted(n * sizeof(double)), small(16);
-    double* c = static_cast<double*>(cols.p);
+    Scratch cols(n * 4 * sizeof(unsigned long long)), alt(n * sizeof(unsigned long long)), small(16),
+        tmp(radix_tmp_bytes(n));
+    unsigned long long* c = static_cast<unsigned long long*>(cols.p);
     unsigned long long* pb = static_cast<unsigned long long*>(small.p);
     SPHRAY_CUDA_OK(cudaMemsetAsync(small.p, 0, 16, s));
     k_stats_columns<<<grid_for(n, 256), 256, 0, s>>>(pxyzh, mvr, n, c, c + n, c + 2 * n, c + 3 * n, pb,
                                                      reinterpret_cast<unsigned int*>(pb + 1));
     SPHRAY_CUDA_OK(cudaGetLastError());
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, bytes, static_cast<const double*>(nullptr),
-                                   static_cast<double*>(nullptr), static_cast<int64_t>(n), 0,
-                                   static_cast<int>(sizeof(double) * 8), s);
-    Scratch tmp(bytes);
-    double* out = static_cast<double*>(sorted.p);
+    unsigned long long* other = static_cast<unsigned long long*>(alt.p);
     for (int k = 0; k < 4; ++k) {
-        // medians of sorted columns (detail::median, quantize.hpp:118-122); the
-        // radix order equals std::sort's except for the relative order of -0.0
-        // and +0.0, which compare equal
-        SPHRAY_CUDA_OK(cub::DeviceRadixSort::SortKeys(tmp.p, bytes, c + k * n, out,
-                                                      static_cast<int64_t>(n), 0,
-                                                      static_cast<int>(sizeof(double) * 8), s));
-        double mid[2] = {0.0, 0.0};
+        // medians of sorted columns (detail::median, quantize.hpp:118-122)
+        unsigned long long* col = c + k * n;
+        const bool in_other = sort_pairs_u64(col, other, nullptr, nullptr, n, 64, tmp.p, s);
+        const unsigned long long* sorted = in_other ? other : col;
+        unsigned long long mid[2] = {0, 0};
         const size_t a = n % 2 ? n / 2 : n / 2 - 1;
-        SPHRAY_CUDA_OK(cudaMemcpyAsync(mid, out + a, (n % 2 ? 1 : 2) * sizeof(double),
+        SPHRAY_CUDA_OK(cudaMemcpyAsync(mid, sorted + a, (n % 2 ? 1 : 2) * sizeof(unsigned long long),
                                        cudaMemcpyDeviceToHost, s));
         SPHRAY_CUDA_OK(cudaStreamSynchronize(s));
-        med[k] = n % 2 ? mid[0] : 0.5 * (mid[0] + mid[1]);
+        double v[2];
+        for (int j = 0; j < 2; ++j) {
+            const unsigned long long u = (mid[j] & 0x8000000000000000ull) ? (mid[j] & ~0x8000000000000000ull) : ~mid[j];
+            std::memcpy(&v[j], &u, sizeof(double));
+        }
+        med[k] = n % 2 ? v[0] : 0.5 * (v[0] + v[1]);
     }
     unsigned long long hb[2] = {0, 0};
     SPHRAY_CUDA_OK(cudaMemcpyAsync(hb, small.p, 16, cudaMemcpyDeviceToHost, s));

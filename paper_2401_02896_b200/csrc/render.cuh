@@ -83,12 +83,17 @@ struct FrameParams {
     unsigned long long* work_counter;
     uint64_t total_work;
     const uint32_t* ray_list;  // retry pass: explicit ray ids (else tile-major)
+    int tile_row0, tile_col0;  // first tile row / column of the frame's work (pixel region)
+    int tiles_wx;              // tile columns of the work
+    int row_lo, row_hi;        // pixels rendered: py in [row_lo, row_hi),
+    int col_lo, col_hi;        //                  px in [col_lo, col_hi)
     uint32_t* retry_list;
     unsigned int* retry_count;
     // output
     double* rgb;  // full image (packed == 0) or owned tiles, tile-major
     int packed;
     unsigned long long* stats;  // StatIndex
+    sphray_ray_record* ray_rec;  // optional per-ray records, index (py - row_lo) * W + px
     // validation dumps (optional)
     unsigned long long* dump_count;  // [0] hits [1] pieces
     uint64_t dump_cap_hits, dump_cap_pieces;
@@ -110,6 +115,8 @@ enum StatIndex {
     kStatMaxPending = 5,
     kStatOverflowKey = 6,
     kStatSkipped = 7,
+    kStatTerminated = 29,  // rays that reached T <= 1e-3 (early ray termination)
+    kStatAccumOverflowRay = 30,  // smallest ray whose merged coefficients left int64 (min; ~0: none)
     // work counters, filled only in -DSPHRAY_KSTATS=1 builds (diagnostics)
     kStatFlushes = 8,
     kStatScanned = 9,   // pending entries examined by flush selection
@@ -122,7 +129,7 @@ enum StatIndex {
     kStatGather = 16,    // 32-candidate gather iterations
     kStatPeak0 = 17,     // rays by largest post-flush residual: <128, <192, <256, <320, <384, >=384
     kStatBits0 = 23,     // flushes by sort-key bits: <=8, <=10, <=12, <=14, <=16, >16
-    kStatCount = 29
+    kStatCount = 31
 };
 constexpr int kStatFirstK = kStatFlushes;
 
@@ -166,10 +173,15 @@ void device_dataset_stats(const double4* pxyzh, const double4* mvr, size_t n, cu
                           double med[4], double* phi_max, bool* bad);
 void launch_render(const FrameParams& P, int D, int m, int blocks, int warps, cudaStream_t s);
 void launch_prep(const PrepParams& p, cudaStream_t s);
-void launch_emit(const PrepParams& p, const uint32_t* offsets, unsigned long long* keys,
+// depth order of the particles: keys = orderable(front), vals = index
+void launch_depth_keys(const float* front, int n, uint32_t* keys, uint32_t* vals, cudaStream_t s);
+// counts in depth order; *total (device, zeroed by the caller) += their sum
+void launch_gather_counts(const uint32_t* counts, const uint32_t* order, int n, uint32_t* out,
+                          unsigned long long* total, cudaStream_t s);
+// (tile, particle) entries, particles visited in depth order
+void launch_emit(const PrepParams& p, const uint32_t* order, const uint32_t* offsets, uint32_t* keys,
                  uint32_t* vals, cudaStream_t s);
-void launch_tile_ranges(const unsigned long long* keys, size_t m, uint32_t* begin, uint32_t* end,
-                        cudaStream_t s);
+void launch_tile_ranges(const uint32_t* keys, size_t m, uint32_t* begin, uint32_t* end, cudaStream_t s);
 void launch_reach(const CamConst& cam, int n, double q, const double4* pxyzh, const int4* bbox,
                   unsigned long long* skipped, cudaStream_t s);
 void launch_unpack(const double* packed, size_t per_rank, int nranks, int tiles_x, int W, int H,
@@ -185,10 +197,14 @@ void launch_quantize_hits(const QuantParams& Q, int D, const sphray_particle* ps
                           const double* tchi, const double* lam, int64_t* knot_t,
                           int64_t* knot_b, int32_t* knot_count, cudaStream_t s);
 
-size_t cub_scan_bytes(size_t n);
-void cub_scan(const uint32_t* in, uint32_t* out, size_t n, void* tmp, size_t bytes, cudaStream_t s);
-size_t cub_sort_bytes(size_t n, int end_bit);
-void cub_sort(const unsigned long long* kin, unsigned long long* kout, const uint32_t* vin,
-              uint32_t* vout, size_t n, int end_bit, void* tmp, size_t bytes, cudaStream_t s);
+// sort.cu: hand-written scan and stable LSD radix sort
+size_t scan_tmp_bytes(size_t n);
+void scan_u32(const uint32_t* in, uint32_t* out, size_t n, void* tmp, uint32_t* total_dev, cudaStream_t s);
+size_t radix_tmp_bytes(size_t n);
+int radix_passes(int end_bit);
+bool sort_pairs_u64(unsigned long long* kin, unsigned long long* kout, uint32_t* vin, uint32_t* vout,
+                    size_t n, int end_bit, void* tmp, cudaStream_t s);
+bool sort_pairs_u32(uint32_t* kin, uint32_t* kout, uint32_t* vin, uint32_t* vout, size_t n, int end_bit,
+                    void* tmp, cudaStream_t s);
 
 }  // namespace sphray_b200

@@ -138,14 +138,74 @@ __device__ __forceinline__ int sample_count(double len, double step, double inv_
     return c > 2.0 ? static_cast<int>(c) : 2;
 }
 
-// alpha = 1 - exp(-x) (raycast.hpp:372): a 4-term series below 0.05 (error
-// < x^5/120 < 3e-9), fp32 exp above (relative error ~1e-7 there, no
-// cancellation); both far inside the stated 1e-4 RGB tolerance.
+// alpha = 1 - exp(-x) (raycast.hpp:372) in fp64: below 1/16 the Taylor series
+// of 1 - e^-x to x^8 (truncation < x^9/9! < 2e-17 relative), else
+// 1 - exp(-x) as the reference writes it (CUDA's exp is within 1 ulp of
+// glibc's).  Either way alpha is within a few ulps of the reference's, so the
+// early-termination test T <= 1e-3 sees the same transmittance to ~1e-15.
 __device__ __forceinline__ double alpha_of(double x) {
-    if (x < 0.05) return x * (1.0 - x * (0.5 - x * (1.0 / 6.0 - x * (1.0 / 24.0))));
-    return 1.0 - static_cast<double>(__expf(-static_cast<float>(x)));
+    if (x < 0.0625) {
+        double s = 1.0 / 40320.0;
+        s = fma(s, -x, 1.0 / 5040.0);
+        s = fma(s, -x, 1.0 / 720.0);
+        s = fma(s, -x, 1.0 / 120.0);
+        s = fma(s, -x, 1.0 / 24.0);
+        s = fma(s, -x, 1.0 / 6.0);
+        s = fma(s, -x, 0.5);
+        s = fma(s, -x, 1.0);
+        return s * x;
+    }
+    return 1.0 - exp(-x);
 }
 
+// sphray_piece_mix (include/sphray_gpu.h) of one FieldPiece, for the per-ray
+// piece checksum of sphray_ray_record.
+template <int D>
+__device__ __forceinline__ uint64_t piece_mix(int64_t t, const uint64_t (&a)[D + 1]) {
+    constexpr uint64_t M[8] = {0x9E3779B97F4A7C15ull, 0xC2B2AE3D27D4EB4Full, 0x165667B19E3779F9ull,
+                               0x27D4EB2F165667C5ull, 0x94D049BB133111EBull, 0xBF58476D1CE4E5B9ull,
+                               0xD6E8FEB86659FD93ull, 0xFF51AFD7ED558CCDull};
+    uint64_t x = static_cast<uint64_t>(t) * M[0];
+#pragma unroll
+    for (int d = 0; d <= D; ++d) x += a[d] * M[d + 1];
+    x ^= x >> 31;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 29;
+    return x;
+}
+
+// Genuine-overflow test of one Taylor shift (RayAccumulator::advance,
+// raycast.hpp:232-249).  The merge runs modulo 2^64, which equals the exact
+// (Int128) result whenever the exact coefficients fit int64.
+// Given an exact input polynomial v (as doubles) and the wrapped result w of
+// shifting it by delta, the exact result is predicted in fp64 (relative error
+// ~2^-50 of the terms); |prediction - w| >= 2^62 means the exact coefficient
+// left int64 -- the case where render_scene<int64_t> throws OverflowError and
+// a wrapped merge would silently give a wrong field.  A non-finite prediction
+// (astronomic terms) counts as overflow too.
+template <int D>
+__device__ __forceinline__ bool shift_overflows(const double (&v)[D + 1], double delta,
+                                                const uint64_t (&w)[D + 1]) {
+    double p[D + 1];
+#pragma unroll
+    for (int d = 0; d <= D; ++d) p[d] = v[d];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = D - 1; j >= i; --j) p[j] = fma(delta, p[j + 1], p[j]);
+    bool bad = false;
+#pragma unroll
+    for (int d = 0; d <= D; ++d)
+        bad |= !(fabs(p[d] - static_cast<double>(static_cast<int64_t>(w[d]))) < 0x1p62);
+    return bad;
+}
+
+// a += j modulo 2^64, flagging signed overflow (Checked<int64_t> +, int_ops.hpp:73-80)
+__device__ __forceinline__ uint64_t add_checked(uint64_t a, uint64_t j, bool& o) {
+    const uint64_t r = a + j;
+    o |= static_cast<int64_t>((a ^ r) & (j ^ r)) < 0;
+    return r;
+}
 
 struct WarpMem {
     uint32_t* pt;    // cap: position offsets (see the file comment)
@@ -349,6 +409,8 @@ class RayWorker {
     unsigned long long knots = 0, pieces = 0, hits = 0;
     int max_pending = 0;
     int max_resid = 0;  // SPHRAY_KSTATS: largest pending set left by a flush
+    uint64_t csum = 0;  // per-lane share of the ray's piece checksum (P.ray_rec)
+    bool aovf = false;  // a merged coefficient left int64 (shift_overflows / add_checked)
 
     Compositor<D, TS> cmp;
 
@@ -379,6 +441,8 @@ class RayWorker {
         knots = pieces = hits = 0;
         max_pending = 0;
         max_resid = 0;
+        csum = 0;
+        aovf = false;
         __syncwarp();
     }
 
@@ -402,15 +466,21 @@ class RayWorker {
             const int s = fs[k];
             const int64_t t = tn;
             if (t != tcur) {
-                taylor_shift<D>(Pc, static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur));
+                const uint64_t dl = static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur);
+                double v[D + 1];
+#pragma unroll
+                for (int d = 0; d <= D; ++d) v[d] = static_cast<double>(static_cast<int64_t>(Pc[d]));
+                taylor_shift<D>(Pc, dl);
+                aovf |= shift_overflows<D>(v, static_cast<double>(static_cast<int64_t>(dl)), Pc);
                 tcur = t;
             }
 #pragma unroll
-            for (int d = 1; d <= D; ++d) Pc[d] += pool_c(d, s);
+            for (int d = 1; d <= D; ++d) Pc[d] = add_checked(Pc[d], pool_c(d, s), aovf);
             const bool more = k + 1 < nsel;
             tn = more ? pool_t(fs[k + 1]) : t;
             if (more && tn == t) continue;  // more jumps at this position
             ++npc;
+            if (P.ray_rec && !stop) csum += piece_mix<D>(t, Pc);
             if constexpr (DUMP)
                 if (!stop && P.dump_piece_t) dump_piece(t, Pc);
             if (!more) {
@@ -491,6 +561,30 @@ class RayWorker {
         for (int d = 0; d <= D; ++d) Pc[d] = E[d];
         walk(k0, k1, nsel, Pc, comp, false, lead, ot, oa, Tl, cr, cg, cb, npc, nsmp);
         __syncwarp();
+        // Overflow test of each run's first shift (the walk tests the rest):
+        // the state entering lane l's run (every jump before it, taken from the
+        // scan) must be the exact shift of lane l-1's end state -- or, for
+        // lane 0, of the previous flush's open piece.
+        {
+            const int64_t tlast = k1 > k0 ? pool_t(fs[k1 - 1]) : 0;
+            int64_t tp = static_cast<int64_t>(__shfl_up_sync(kFull, static_cast<unsigned long long>(tlast), 1));
+            double v[D + 1];
+#pragma unroll
+            for (int d = 0; d <= D; ++d) {
+                const uint64_t up = __shfl_up_sync(kFull, static_cast<unsigned long long>(Pc[d]), 1);
+                v[d] = static_cast<double>(static_cast<int64_t>(lane == 0 ? oa[d] : up));
+            }
+            if (lane == 0) tp = ot;
+            if (k0 < k1 && (lane > 0 || lead)) {
+                const int64_t t0 = pool_t(fs[k0]);
+                uint64_t Ps[D + 1];
+#pragma unroll
+                for (int d = 0; d <= D; ++d) Ps[d] = E[d];
+                taylor_shift<D>(Ps, static_cast<uint64_t>(t0) - static_cast<uint64_t>(tref));
+                aovf |= shift_overflows<D>(
+                    v, static_cast<double>(static_cast<int64_t>(static_cast<uint64_t>(t0) - static_cast<uint64_t>(tp))), Ps);
+            }
+        }
         has_open = true;
         pieces += __reduce_add_sync(kFull, static_cast<unsigned>(npc));
         if (SPHRAY_KSTATS) {
@@ -878,8 +972,15 @@ class RayWorker {
         return true;
     }
 
-    __device__ void finish(double* out) {
+    __device__ void finish(double* out, int px, int py) {
         const double sr = warp_sum(Cr), sg = warp_sum(Cg), sb = warp_sum(Cb);
+        const bool ovf_any = __any_sync(kFull, aovf);
+        uint64_t cs = 0;
+        if (P.ray_rec) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(kFull, csum, o);
+            cs = csum;
+        }
         if (lane == 0) {
             double r = P.bg[0], g = P.bg[1], b = P.bg[2];
             if (knots > 0) {
@@ -908,8 +1009,20 @@ class RayWorker {
                 atomicAdd(&P.stats[kStatIntOps], ops);
                 if (residual) atomicAdd(&P.stats[kStatResidual], 1ull);
             }
+            if (term) atomicAdd(&P.stats[kStatTerminated], 1ull);
+            if (ovf_any) atomicMin(&P.stats[kStatAccumOverflowRay], static_cast<unsigned long long>(ray_id));
             if (hits) atomicAdd(&P.stats[kStatHits], hits);
             atomicMax(&P.stats[kStatMaxPending], static_cast<unsigned long long>(max_pending));
+            if (P.ray_rec) {
+                sphray_ray_record rec;
+                rec.piece_checksum = cs;
+                rec.knots = static_cast<uint32_t>(knots);
+                rec.pieces = static_cast<uint32_t>(pieces);
+                rec.hits = static_cast<uint32_t>(hits);
+                rec.flags = (knots > 0 ? SPHRAY_RAY_TOUCHED : 0u) | (residual ? SPHRAY_RAY_RESIDUAL : 0u) |
+                            (term ? SPHRAY_RAY_TERMINATED : 0u);
+                P.ray_rec[static_cast<size_t>(py - P.row_lo) * (P.col_hi - P.col_lo) + (px - P.col_lo)] = rec;
+            }
             if (SPHRAY_KSTATS) {
                 const int b = max_resid < 128 ? 0 : max_resid < 192 ? 1 : max_resid < 256 ? 2
                             : max_resid < 320 ? 3 : max_resid < 384 ? 4 : 5;
@@ -947,12 +1060,15 @@ __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const __grid_constant_
         } else {
             const uint64_t local = item / kTileRays;
             const int r = static_cast<int>(item % kTileRays);
-            const uint64_t tile = P.nranks > 1 ? local * P.nranks + P.rank : local;
+            const uint64_t tile =
+                P.nranks > 1 ? local * P.nranks + P.rank
+                             : (local / P.tiles_wx + P.tile_row0) * static_cast<uint64_t>(P.tiles_x) +
+                                   P.tile_col0 + local % P.tiles_wx;
             const int tx = static_cast<int>(tile % P.tiles_x), ty = static_cast<int>(tile / P.tiles_x);
             px = tx * kTile + (r & (kTile - 1));
             py = ty * kTile + (r >> kTileShift);
         }
-        if (px >= P.cam.W || py >= P.cam.H) continue;
+        if (px >= P.col_hi || px < P.col_lo || py >= P.row_hi || py < P.row_lo) continue;
         rw.ray_id = static_cast<uint64_t>(py) * P.cam.W + px;
         uint64_t out_index = rw.ray_id;
         if (P.packed) {
@@ -960,7 +1076,7 @@ __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const __grid_constant_
             out_index = (tile / P.nranks) * kTileRays + ((py & (kTile - 1)) << kTileShift) + (px & (kTile - 1));
         }
         if (rw.run(px, py)) {
-            rw.finish(P.rgb + out_index * 3);
+            rw.finish(P.rgb + out_index * 3, px, py);
         } else if (lane == 0) {
             const unsigned at = atomicAdd(P.retry_count, 1u);
             P.retry_list[at] = static_cast<uint32_t>(rw.ray_id);

@@ -80,7 +80,41 @@ def scene_golden(name, ps, cam, tf, lut_path, bg, full=True):
         "rgb", "hit_ray", "knot_t", "pl_piece_t")}, st)
 
 
+def config1_golden():
+    """BASELINE.json config 1 (1e5-particle blob, 256^2, K=4 D=3 N=1024, w64), the
+    one configuration the reference renders whole: the full frame from
+    render_scene<int64_t>, its RenderStats, a digest of the full hit set and the
+    per-ray records of rp_render_region over the whole frame (knots, pieces,
+    hits, residual/termination flags and the checksum of every ray's
+    accumulate<Int128> FieldPieces, sphray_piece_mix)."""
+    ps = ref.generate_scene(1)
+    lut_path = H.lut_path(4, 3, 1024)
+    rl = ref.Lut(lut_path)
+    ds = ref.dataset_stats(ps, rl)
+    qc = ref.choose_quanta(rl, ds)
+    cam = ref.Camera(**H.synth_camera_kwargs(256, 256))
+    rgb, st, _, bits = ref.render_robust(ps, cam, H.SYNTH_TF, rl, qc, ds)
+    _, rec, rst, _, _ = ref.render_region(ps, cam, H.SYNTH_TF, rl, qc, st["step"], 0, 0, 256, 256)
+    for k in ("knots", "rays_touched", "int_ops", "residual_failures"):
+        assert rst[k] == st[k], k
+    ray, pid, lam, tchi = ref.footprint(ps, cam, rl.q)
+    o = np.lexsort((pid, ray))  # ray-major, as the GPU dump returns them
+    out = dict(particles_digest=digest(ps), n_particles=np.array(len(ps)), lut=os.path.basename(lut_path),
+               rgb=rgb, accum_bits=np.array(bits), tau=np.array(qc.tau), sigma=np.array(qc.sigma),
+               h_r=np.array(ds.h_r), a_max=np.array(ds.a_max),
+               n_hits=np.array(len(ray)), digest_hits=digest(ray[o], pid[o], lam[o], tchi[o]),
+               rec_checksum=rec["piece_checksum"], rec_knots=rec["knots"], rec_pieces=rec["pieces"],
+               rec_hits=rec["hits"], rec_flags=rec["flags"],
+               **{"cam_" + k: v for k, v in cam_fields(cam).items()},
+               **{"stat_" + k: np.array(v) for k, v in st.items()})
+    np.savez_compressed(os.path.join(OUT, "config1.npz"), **out)
+    print("config1", st, "hits", len(ray), "bits", bits)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "config1":
+        config1_golden()
+        return
     # the bundled example scene, parsed by the reference's io.hpp loaders
     ps = ref.load_particles(f"{H.REF_DATA}/desk_scene.csv")
     tf = ref.load_tf(f"{H.REF_DATA}/tf.csv")

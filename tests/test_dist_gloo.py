@@ -14,6 +14,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2401_02896_b200 import dist as D
+from tests import dist_layout as DL
 
 
 def _free_port():
@@ -30,11 +31,11 @@ def _worker(rank, world, port, W, H, out_q):
     try:
         rng = np.random.default_rng(1234)
         full = rng.random((H, W, 3))
-        packed = torch.from_numpy(D.pack(full, rank, world))
+        packed = torch.from_numpy(DL.pack(full, rank, world))
         bufs = [torch.empty_like(packed) for _ in range(world)]
         dist.all_gather(bufs, packed)
         gathered = torch.cat(bufs).numpy()
-        img = D.unpack(gathered, world, W, H)
+        img = DL.unpack(gathered, world, W, H)
         ok_img = bool((img == full).all())
         # unique-id broadcast as dist.init_comm does it
         obj = [bytes(range(128)) if rank == 0 else None]
@@ -71,6 +72,24 @@ def test_pack_unpack_roundtrip(nranks):
     rng = np.random.default_rng(nranks)
     img = rng.random((45, 61, 3))
     nt = D.tile_grid(61, 45)[2]
-    gathered = np.concatenate([D.pack(img, r, nranks) for r in range(nranks)])
-    assert (D.unpack(gathered, nranks, 61, 45) == img).all()
+    gathered = np.concatenate([DL.pack(img, r, nranks) for r in range(nranks)])
+    assert (DL.unpack(gathered, nranks, 61, 45) == img).all()
     assert sum(len(D.owned_tiles(r, nranks, nt)) for r in range(nranks)) == nt
+
+
+def test_bench_launches_its_ranks():
+    """`bench.py --gpus 2` started without a launcher re-executes itself under
+    torch.distributed.run (one process per rank); the line reports n_gpus 2."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["ranks_ms_max"] == 2.0

@@ -265,7 +265,7 @@ def test_sharded_tiles_match_single_gpu(name, nranks):
     into its packed buffer (the kernel's packed write path); gathered and
     unpacked with the layout k_unpack uses, the image is bit-identical to the
     single-rank render, and the per-rank counters sum to the same totals."""
-    from paper_2401_02896_b200 import dist as SD
+    from tests import dist_layout as SD
 
     g = load(name)
     lut = S.load_lut(g["lut_path"])
