@@ -355,7 +355,7 @@ def run_ours(args):
         # the timed frame (the full image on rank 0 after the tile gather)
         class _Dev:  # the library's device image, viewed through __cuda_array_interface__
             __cuda_array_interface__ = {"shape": (res, res, 3), "typestr": "<f8",
-                                        "data": (ctx.device_image_ptr(), True), "version": 3}
+                                        "data": (ctx.device_image_ptr(), False), "version": 3}
         torch.cuda.synchronize()
         frame = torch.as_tensor(_Dev(), device="cuda").cpu().numpy()
     image_sha = hashlib.sha256(frame.tobytes()).hexdigest() if frame is not None else None

@@ -341,6 +341,27 @@ sphray_status sphray_choose_quanta(const sphray_lut_view* lut, const sphray_data
                                    int int_width, double kappa, double kappa_prime,
                                    sphray_quanta* out, sphray_error* err);
 
+/* serialize_lut / save_lut (lut.hpp:335-352, 395-399): the .splt file image of
+ * a LUT view (kernel_id: up to 16 bytes, e.g. "cubic-bspline").  Two-call
+ * protocol on cap for sphray_lut_serialize. */
+sphray_status sphray_lut_serialize(const sphray_lut_view* lut, const char* kernel_id, uint8_t* out,
+                                   size_t cap, size_t* nbytes, sphray_error* err);
+sphray_status sphray_lut_save(const char* path, const sphray_lut_view* lut, const char* kernel_id,
+                              sphray_error* err);
+
+/* The reference CLI's render report (sphray_main.cpp:196-256), written next to
+ * the image as "<out>.json": quanta, RenderStats, dataset statistics, errors
+ * {E_star (overall_error, lut.hpp:284-290), Q_D (quantization_error,
+ * quantize.hpp:64-73), combined}, overflow_count, K, D, kernel, seed, image --
+ * the same JSON text (2-space indent).  stats == NULL or stats->particles == 0
+ * gives the reference's empty-scene report.  kappa/kappa_prime <= 0 select the
+ * cubic B-spline's constants.  Two-call protocol on cap (len excludes the NUL). */
+sphray_status sphray_render_report(const sphray_lut_view* lut, const char* kernel_id,
+                                   const sphray_dataset_stats* ds, const sphray_quanta* qc,
+                                   const sphray_render_stats* stats, uint64_t seed,
+                                   const char* image_path, double kappa, double kappa_prime,
+                                   char* out, size_t cap, size_t* len, sphray_error* err);
+
 /* .splt parsing (lut.hpp:354-393): validates the file image and copies the
  * header fields into *view.  view->records points into `bytes` (offset 44) when
  * that address is 8-byte aligned, else it is NULL and the caller supplies an

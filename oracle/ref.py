@@ -104,6 +104,7 @@ def lib():
         _lib.rp_load_particles.restype = C.c_int64
         _lib.rp_load_tf.restype = C.c_int64
         _lib.rp_scene_default_count.restype = C.c_size_t
+        _lib.rp_render_report.restype = C.c_int64
     return _lib
 
 
@@ -468,3 +469,20 @@ def piece_mix(t, a, D: int) -> np.ndarray:
         x = x * np.uint64(0xBF58476D1CE4E5B9)
         x = x ^ (x >> np.uint64(29))
     return x
+
+
+def render_report(particles, cam: Camera, tf, lut: Lut, int_width: int = 64, seed: int = 0,
+                  image: str = "") -> str:
+    """The reference CLI's render report JSON text (rp_render_report)."""
+    a = as_particles(particles)
+    c = cam.c()
+    tfa, ntf = _tf(tf)
+    err = RpError()
+    args = (_pp(a), C.c_size_t(len(a)), C.byref(c), tfa, C.c_size_t(ntf), C.c_void_p(lut.h),
+            int_width, C.c_uint64(seed), image.encode())
+    n = lib().rp_render_report(*args, None, C.c_size_t(0), C.byref(err))
+    if n < 0:
+        raise RefError(err)
+    buf = C.create_string_buffer(n + 1)
+    lib().rp_render_report(*args, buf, C.c_size_t(n + 1), C.byref(err))
+    return buf.value.decode()

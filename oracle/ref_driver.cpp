@@ -804,6 +804,75 @@ int rp_render_region(const rp_particle* ps, std::size_t n, const rp_camera* c,
     });
 }
 
+// The reference CLI's render report (sphray_main.cpp:196-256): the CLI does
+// not build here (CLI11 absent), so this restates the report construction of
+// cmd_render around the reference's own render_scene<Int>, dataset_stats,
+// choose_quanta, overall_error and quantization_error.  Writes the JSON text
+// (dump(2) + newline) to out (cap bytes incl. NUL); returns its length.
+std::int64_t rp_render_report(const rp_particle* ps, std::size_t n, const rp_camera* c,
+                              const rp_tf_point* tfp, std::size_t ntf, void* lutp, int int_width,
+                              std::uint64_t seed, const char* image, char* out, std::size_t cap,
+                              rp_error* err) {
+    std::string txt;
+    const int rc = guarded(err, [&] {
+        const Camera cam = to_cam(c);
+        cam.validate();
+        const TransferFunction tf = to_tf(tfp, ntf);
+        const auto kernel = cubic_bspline();
+        const auto width = int_width_from(int_width);
+        nlohmann::json report;
+        const std::span<const Particle> particles = to_span(ps, n);
+        if (particles.empty()) {
+            report["quanta"] = nullptr;
+            report["stats"] = {{"particles", 0}, {"knots", 0}, {"rays_touched", 0}};
+            report["errors"] = nullptr;
+            report["overflow_count"] = 0;
+        } else {
+            const Lut& lut = *static_cast<Lut*>(lutp);
+            const auto cc = kernel_constants(kernel);
+            const ApproxConfig cfg{lut.K, lut.D};
+            const auto stats = dataset_stats(particles, lut);
+            const auto qc = choose_quanta(cfg, cc, kernel.q, stats, width);
+            RenderOptions opts;
+            RenderStats rs;
+            (void)dispatch_int_width(width, [&](auto tag) {
+                using Int = typename decltype(tag)::type;
+                return render_scene<Int>(particles, cam, tf, lut, qc, stats, opts, &rs);
+            });
+            const double estar = overall_error(lut, cc);
+            const double qd = quantization_error(cfg, cc, kernel.q, qc.tau / stats.h_r, qc.sigma / stats.phi_repr);
+            report["quanta"] = {{"tau", qc.tau}, {"sigma", qc.sigma}, {"int_width", int_width}};
+            report["stats"] = {{"particles", rs.particles},
+                               {"skipped_particles", rs.skipped_particles},
+                               {"knots", rs.knots},
+                               {"rays_touched", rs.rays_touched},
+                               {"int_ops", rs.int_ops},
+                               {"residual_failures", rs.residual_failures},
+                               {"step", rs.step}};
+            report["dataset"] = {{"count", stats.count},
+                                 {"h_r", stats.h_r},
+                                 {"phi_repr", stats.phi_repr},
+                                 {"a_max", stats.a_max},
+                                 {"clustering_factor", stats.clustering_factor}};
+            report["errors"] = {{"E_star", estar}, {"Q_D", qd}, {"combined", std::hypot(estar, qd)}};
+            report["overflow_count"] = 0;
+            report["K"] = lut.K;
+            report["D"] = lut.D;
+        }
+        report["kernel"] = kernel.id;
+        report["seed"] = seed;
+        report["image"] = image ? image : "";
+        txt = report.dump(2) + "\n";
+    });
+    if (rc) return -1;
+    if (out && cap) {
+        const std::size_t k = std::min(cap - 1, txt.size());
+        std::memcpy(out, txt.data(), k);
+        out[k] = 0;
+    }
+    return static_cast<std::int64_t>(txt.size());
+}
+
 int rp_generate_scene(int config, std::size_t n, std::uint64_t seed, rp_particle* out, rp_error* err) {
     return guarded(err, [&] {
         if (sphray_scenes::default_count(config) == 0) throw ConfigError("unknown scene config");

@@ -224,6 +224,12 @@ def load_library():
                                        P(_Quanta), P(_Error)]
     L.sphray_lut_parse.argtypes = [C.c_void_p, C.c_size_t, P(_LutView), C.c_char_p, P(_Error)]
     L.sphray_generate_scene.argtypes = [C.c_int, C.c_size_t, C.c_uint64, P(_Particle), P(_Error)]
+    L.sphray_lut_serialize.argtypes = [P(_LutView), C.c_char_p, C.c_void_p, C.c_size_t, P(C.c_size_t),
+                                       P(_Error)]
+    L.sphray_lut_save.argtypes = [C.c_char_p, P(_LutView), C.c_char_p, P(_Error)]
+    L.sphray_render_report.argtypes = [P(_LutView), C.c_char_p, P(_DStats), P(_Quanta), P(_RStats),
+                                       C.c_uint64, C.c_char_p, C.c_double, C.c_double, C.c_char_p,
+                                       C.c_size_t, P(C.c_size_t), P(_Error)]
     L.sphray_scene_default_count.argtypes = [C.c_int]
     L.sphray_scene_default_count.restype = C.c_size_t
     for name in ("sphray_context_create", "sphray_comm_unique_id", "sphray_context_init_comm",
@@ -232,7 +238,8 @@ def load_library():
                  "sphray_render_scene", "sphray_scene_upload", "sphray_scene_render",
                  "sphray_scene_hits", "sphray_scene_pieces", "sphray_quantize_hits",
                  "sphray_compute_dataset_stats", "sphray_choose_quanta", "sphray_lut_parse",
-                 "sphray_generate_scene"):
+                 "sphray_generate_scene", "sphray_lut_serialize", "sphray_lut_save",
+                 "sphray_render_report"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -414,6 +421,38 @@ class Lut:
     def records(self) -> np.ndarray:
         m, nj = (self.K + 1) // 2, self.K * self.D // 2
         return self._records.reshape(self.N, 2 + m + nj)
+
+    def serialize(self) -> bytes:
+        """serialize_lut (lut.hpp:335-352): the .splt file image."""
+        L = load_library()
+        n, err = C.c_size_t(), _Error()
+        kid = self.kernel_id.encode()
+        _check(L.sphray_lut_serialize(C.byref(self._view), kid, None, 0, C.byref(n), C.byref(err)), err)
+        out = (C.c_uint8 * n.value)()
+        _check(L.sphray_lut_serialize(C.byref(self._view), kid, out, n.value, C.byref(n), C.byref(err)), err)
+        return bytes(out)
+
+
+def save_lut(lut: "Lut", path: str) -> None:
+    """save_lut (lut.hpp:395-399)."""
+    L = load_library()
+    err = _Error()
+    _check(L.sphray_lut_save(os.fsencode(path), C.byref(lut.view), lut.kernel_id.encode(), C.byref(err)), err)
+
+
+def render_report(lut: "Lut", stats: "DatasetStats", qc: "QuantaConfig", rstats: "RenderStats",
+                  seed: int = 0, image: str = "") -> str:
+    """The reference CLI's `render` report JSON (sphray_main.cpp:196-256)."""
+    L = load_library()
+    ds, q = stats._c(), qc._c()
+    rs = _RStats(**{f: getattr(rstats, f) for f, _ in _RStats._fields_}) if rstats is not None else None
+    n, err = C.c_size_t(), _Error()
+    args = (C.byref(lut.view), lut.kernel_id.encode(), C.byref(ds), C.byref(q),
+            C.byref(rs) if rs is not None else None, C.c_uint64(seed), image.encode(), 0.0, 0.0)
+    _check(L.sphray_render_report(*args, None, 0, C.byref(n), C.byref(err)), err)
+    buf = C.create_string_buffer(n.value + 1)
+    _check(L.sphray_render_report(*args, buf, n.value + 1, C.byref(n), C.byref(err)), err)
+    return buf.value.decode()
 
 
 def load_lut(path: str) -> Lut:

@@ -1,6 +1,7 @@
 // api.cpp -- the extern "C" boundary (include/sphray_gpu.h).  Exceptions never
 // cross it: every entry point converts to a status code + sphray_error.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -361,8 +362,16 @@ sphray_status sphray_scene_upload_file(sphray_context* ctx, const char* path,
                                        const sphray_lut_view* lut, sphray_error* err) {
     return guarded(err, [&] {
         if (!ctx || !path || !lut) fail(SPHRAY_ERR_CONFIG, "null argument");
-        const auto ps = load_particles(path);
-        ctx->engine->upload_scene(ps.data(), ps.size(), *lut);
+        Engine& e = engine(ctx);
+        if (is_sprt(path)) {
+            // SPRT records land directly in pinned host memory (no pageable bounce)
+            sphray_particle* stage = nullptr;
+            const size_t n = read_sprt_into(path, [&](size_t k) { return stage = e.stage_particles(k); });
+            e.upload_scene(stage, n, *lut);
+        } else {
+            const auto ps = load_particles(path);
+            e.upload_scene(ps.data(), ps.size(), *lut);
+        }
     });
 }
 
@@ -371,6 +380,48 @@ sphray_status sphray_scene_dataset_stats(sphray_context* ctx, double clustering_
     return guarded(err, [&] {
         if (!ctx || !out) fail(SPHRAY_ERR_CONFIG, "null context/output");
         *out = ctx->engine->scene_dataset_stats(clustering_factor);
+    });
+}
+
+sphray_status sphray_lut_serialize(const sphray_lut_view* lut, const char* kernel_id, uint8_t* out,
+                                   size_t cap, size_t* nbytes, sphray_error* err) {
+    return guarded(err, [&] {
+        if (!lut) fail(SPHRAY_ERR_CONFIG, "null LUT view");
+        const auto bytes = serialize_lut(*lut, kernel_id ? kernel_id : "");
+        if (nbytes) *nbytes = bytes.size();
+        if (out && cap) std::memcpy(out, bytes.data(), std::min(cap, bytes.size()));
+    });
+}
+
+sphray_status sphray_lut_save(const char* path, const sphray_lut_view* lut, const char* kernel_id,
+                              sphray_error* err) {
+    return guarded(err, [&] {
+        if (!lut || !path) fail(SPHRAY_ERR_CONFIG, "null argument");
+        const auto bytes = serialize_lut(*lut, kernel_id ? kernel_id : "");
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f) fail(SPHRAY_ERR_IO, std::string("lut: cannot open ") + path + " for writing");
+        const size_t w = std::fwrite(bytes.data(), 1, bytes.size(), f);
+        const int c = std::fclose(f);
+        if (w != bytes.size() || c != 0) fail(SPHRAY_ERR_IO, "lut: write failure");
+    });
+}
+
+sphray_status sphray_render_report(const sphray_lut_view* lut, const char* kernel_id,
+                                   const sphray_dataset_stats* ds, const sphray_quanta* qc,
+                                   const sphray_render_stats* stats, uint64_t seed,
+                                   const char* image_path, double kappa, double kappa_prime,
+                                   char* out, size_t cap, size_t* len, sphray_error* err) {
+    return guarded(err, [&] {
+        if (!(kappa > 0.0)) kappa = kCubicKappa;
+        if (!(kappa_prime > 0.0)) kappa_prime = kCubicKappaPrime;
+        const std::string txt = render_report_json(lut, kernel_id ? kernel_id : "", ds, qc, stats, seed,
+                                                   image_path ? image_path : "", kappa, kappa_prime);
+        if (len) *len = txt.size();
+        if (out && cap) {
+            const size_t k = std::min(cap - 1, txt.size());
+            std::memcpy(out, txt.data(), k);
+            out[k] = 0;
+        }
     });
 }
 

@@ -218,6 +218,15 @@ __device__ __forceinline__ int64_t cneg(int64_t a, bool& o) {
     return static_cast<int64_t>(0ull - static_cast<uint64_t>(a));
 }
 
+// Checked<int32_t> (int_ops.hpp:63-99) on top of the int64 arithmetic: every
+// int32 operation's operands fit int32, so its exact result is the int64 one;
+// `on` flags any result outside int32 (round_to_int<int32_t>'s range check is
+// the same test).
+__device__ __forceinline__ int64_t narrow32(int64_t v, bool on, bool& o) {
+    if (on) o |= v != static_cast<int64_t>(static_cast<int32_t>(v));
+    return v;
+}
+
 // round_to_int<int64_t> (int_ops.hpp:103-110): nearbyint (ties to even),
 // then the range check [-2^63, 2^63).
 __device__ __forceinline__ int64_t round_checked(double x, bool& o) {

@@ -147,6 +147,12 @@ Engine::~Engine() {
 
 void Engine::set_device() const { CUDA_OK(cudaSetDevice(device_)); }
 
+sphray_particle* Engine::stage_particles(size_t n) {
+    set_device();
+    h_stage_.ensure(std::max<size_t>(n, 1) * sizeof(sphray_particle));
+    return static_cast<sphray_particle*>(h_stage_.p);
+}
+
 void Engine::init_comm(int rank, int nranks, const uint8_t id[128]) {
     set_device();
     if (nranks < 1 || rank < 0 || rank >= nranks) fail(SPHRAY_ERR_CONFIG, "bad rank / nranks");
@@ -438,6 +444,7 @@ void Engine::validate(const sphray_camera& cam, const sphray_quanta& qc,
         Q.sigma = qc.sigma;
         Q.inv_tau = recip_or_nan(qc.tau);
         Q.inv_dl = recip_or_nan(lut_.delta_lambda);
+        Q.w32 = qc.int_width == 32;
         launch_quantize_hits(Q, D, dps.as<sphray_particle>(), dpw.as<double>(), dpt.as<double>(), nh,
                              dtc.as<double>(), dla.as<double>(), dkt.as<int64_t>(), dkb.as<int64_t>(),
                              dkc.as<int32_t>(), s);
@@ -505,17 +512,9 @@ void Engine::validate(const sphray_camera& cam, const sphray_quanta& qc,
 
     // group 3: dense-L2 envelope on the first 64 rays (ray-id order)
     {
-        double acc = 0.0;
-        const double dl = lut_.delta_lambda;
-        for (int e = 0; e < lut_.N; ++e) acc += lut_.lambda[e] * lut_.error[e] * lut_.error[e] * dl;
-        const double estar = std::sqrt(2.0 * M_PI * acc) / kCubicKappa;      // lut.hpp:284-290
-        const double tq = qc.tau / ds.h_r, sq = qc.sigma / ds.phi_repr;       // quantize.hpp:64-73
-        if (!(tq > 0.0)) fail(SPHRAY_ERR_CONFIG, "quantization_error: tau must be positive");
-        if (!(sq >= 0.0)) fail(SPHRAY_ERR_CONFIG, "quantization_error: sigma must be nonnegative");
-        double sacc = kCubicKappaPrime * kCubicKappaPrime * tq * tq;
-        for (int k = 0; k <= D; ++k)
-            sacc += 2.0 * std::pow(lut_.q, 2 * k + 3) / ((2 * k + 1) * (2 * k + 3)) * sq * sq / std::pow(tq, 2 * k);
-        const double qd = std::sqrt(sacc) / (4.0 * kCubicKappa);
+        const double estar = overall_error(lut_, kCubicKappa);                   // lut.hpp:284-290
+        const double qd = quantization_error(lut_, kCubicKappa, kCubicKappaPrime, qc.tau / ds.h_r,
+                                             qc.sigma / ds.phi_repr);            // quantize.hpp:64-73
         rep->l2_envelope = 4.0 * std::hypot(estar, qd);
         // h_min over the particles
         std::vector<double4> hx(n_);
@@ -605,10 +604,12 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     const CamConst C = make_camera(cam);  // render_scene: cam.validate() (raycast.hpp:419)
     validate_tf(tf, ntf);                 // raycast.hpp:420
     if (!has_scene_) fail(SPHRAY_ERR_CONFIG, "no scene uploaded");
-    if (qc.int_width != 64)
+    if (qc.int_width != 64 && qc.int_width != 32)
         fail(SPHRAY_ERR_CONFIG,
-             "the B200 path computes with int64 quanta (int_width 64); widths 32/128 are not "
-             "supported yet");
+             "int_width " + std::to_string(qc.int_width) +
+                 ": the B200 path serves render_scene<int32_t> and <int64_t> (128-bit quanta are "
+                 "not supported)");
+    const bool w32 = qc.int_width == 32;
     const int D = lut_.D, m = lut_.m;
     const double step = opts.step > 0.0 ? opts.step : ds.h_r / 8.0;  // raycast.hpp:424
     const int W = C.W, H = C.H;
@@ -755,10 +756,15 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
             const int end_bit = bits_for(owned_max);
             const bool k2 = sort_pairs_u32(d_keys_.as<uint32_t>(), d_keys2_.as<uint32_t>(), d_vals_.as<uint32_t>(),
                                            d_vals2_.as<uint32_t>(), entries, end_bit, d_tmp_.p, s);
-            cand_ = k2 ? d_vals2_.as<uint32_t>() : d_vals_.as<uint32_t>();
-            launch_tile_ranges(k2 ? d_keys2_.as<uint32_t>() : d_keys_.as<uint32_t>(), entries,
-                               d_tile_begin_.as<uint32_t>(), d_tile_end_.as<uint32_t>(), s);
-            launches += 1 + 3 * radix_passes(end_bit) + 1;  // emit, sort, ranges
+            const uint32_t* cand = k2 ? d_vals2_.as<uint32_t>() : d_vals_.as<uint32_t>();
+            const uint32_t* tkeys = k2 ? d_keys2_.as<uint32_t>() : d_keys_.as<uint32_t>();
+            launch_tile_ranges(tkeys, entries, d_tile_begin_.as<uint32_t>(), d_tile_end_.as<uint32_t>(), s);
+            d_cxyzh_.ensure(entries * sizeof(double4));
+            d_cmeta_.ensure(entries * sizeof(uint4));
+            launch_records(tkeys, cand, entries, d_pxyzh_.as<double4>(), d_bbox_.as<int4>(),
+                           d_front_.as<float>(), tiles_x, rank_, nranks_, d_cxyzh_.as<double4>(),
+                           d_cmeta_.as<uint4>(), s);
+            launches += 1 + 3 * radix_passes(end_bit) + 2;  // emit, sort, ranges, records
         }
     }
 
@@ -786,13 +792,15 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     P.Q.sigma = qc.sigma;
     P.Q.inv_tau = recip_or_nan(qc.tau);
     P.Q.inv_dl = recip_or_nan(lut_.delta_lambda);
+    P.Q.w32 = w32 ? 1 : 0;
     P.n = n;
     P.pxyzh = d_pxyzh_.as<double4>();
     P.xy = d_xy_.as<double>();
     P.bbox = d_bbox_.as<int4>();
     P.front = d_front_.as<float>();
     P.orig = d_orig_.as<int32_t>();
-    P.cand = cand_;
+    P.cxyzh = d_cxyzh_.as<double4>();
+    P.cmeta = d_cmeta_.as<uint4>();
     P.tile_begin = d_tile_begin_.as<uint32_t>();
     P.tile_end = d_tile_end_.as<uint32_t>();
     P.tiles_x = tiles_x;
@@ -868,7 +876,9 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     // e.g. degree-1 tables) run the robust variant from the start: it moves
     // the 32-bit window-offset base with every flush.  (The hmax sample above
     // is a heuristic; rays that still overflow go to the robust retry pass.)
-    const bool robust_frame = scene_extent_ / qc.tau > 2147483648.0;
+    // int_width 32 frames run the robust variant too (its quantize and merge
+    // carry the Checked<int32_t> range tests, render_kernel.cuh / quantize.cuh)
+    const bool robust_frame = scene_extent_ / qc.tau > 2147483648.0 || w32;
     P.robust = robust_frame ? 1 : 0;
     const size_t tfb =
         (tfb_full <= 4096 && !dumps && !robust_frame && !std::getenv("SPHRAY_TF_GLOBAL")) ? tfb_full : 0;
@@ -1184,6 +1194,7 @@ void Engine::quantize_hits(const sphray_particle* ps, size_t nhits, const double
     Q.sigma = qc.sigma;
     Q.inv_tau = recip_or_nan(qc.tau);
     Q.inv_dl = recip_or_nan(L.delta_lambda);
+    Q.w32 = qc.int_width == 32;
     launch_quantize_hits(Q, D, dps.as<sphray_particle>(), dpw.as<double>(), dpt.as<double>(), nhits,
                          dtc.as<double>(), dla.as<double>(), dkt.as<int64_t>(), dkb.as<int64_t>(),
                          dkc.as<int32_t>(), stream_);

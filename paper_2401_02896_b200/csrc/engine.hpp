@@ -73,6 +73,9 @@ class Engine {
                        const double* lam, const sphray_lut_view& lut, const sphray_quanta& qc,
                        int64_t* knot_t, int64_t* knot_b, int32_t* knot_count);
     const double* device_image() const { return d_image_.as<double>(); }
+    // pinned host staging for n particle records (file ingestion: the upload
+    // from it is a true async DMA); valid until the next call
+    sphray_particle* stage_particles(size_t n);
     void* stream() const { return stream_; }
     bool has_scene() const { return has_scene_; }
     size_t scene_size() const { return n_; }
@@ -107,7 +110,7 @@ class Engine {
     // frame
     DevBuf d_bbox_, d_front_, d_xy_, d_counts_, d_counts2_, d_offsets_, d_keys_, d_keys2_, d_vals_, d_vals2_;
     DevBuf d_dkeys_, d_dkeys2_, d_order_, d_order2_, d_total_, d_status_;
-    const uint32_t* cand_ = nullptr;  // sorted candidate list of the current frame
+    DevBuf d_cxyzh_, d_cmeta_;  // candidate records of the current frame (tile, front order)
     DevBuf d_tile_begin_, d_tile_end_, d_tf_, d_powtau_, d_image_, d_packed_, d_gather_;
     DevBuf d_stats_, d_work_, d_retry_, d_retry2_, d_retry_count_;
     DevBuf d_dump_count_, d_dump_hr_, d_dump_hp_, d_dump_hl_, d_dump_ht_, d_dump_pr_, d_dump_pt_,

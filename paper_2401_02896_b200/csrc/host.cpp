@@ -337,6 +337,25 @@ namespace {
 double order_weight(double q, int d) {
     return 2.0 * std::pow(q, 2 * d + 3) / ((2 * d + 1) * (2 * d + 3));
 }
+}  // namespace
+
+double overall_error(const LutHost& L, double kappa) {
+    if (kappa <= 0.0) return 0.0;
+    const double dl = L.delta_lambda;
+    double acc = 0.0;
+    for (int e = 0; e < L.N; ++e) acc += L.lambda[e] * L.error[e] * L.error[e] * dl;
+    return std::sqrt(2.0 * std::numbers::pi * acc) / kappa;
+}
+
+double quantization_error(const LutHost& L, double kappa, double kappa_prime, double tau, double sigma) {
+    if (!(tau > 0.0)) fail(SPHRAY_ERR_CONFIG, "quantization_error: tau must be positive");
+    if (!(sigma >= 0.0)) fail(SPHRAY_ERR_CONFIG, "quantization_error: sigma must be nonnegative");
+    double s = kappa_prime * kappa_prime * tau * tau;
+    for (int d = 0; d <= L.D; ++d) s += order_weight(L.q, d) * sigma * sigma / std::pow(tau, 2 * d);
+    return std::sqrt(s) / (4.0 * kappa);
+}
+
+namespace {
 double slope(int D, double kappa, double kappa_prime, double q, double tau, double sigma) {
     double s = 2.0 * kappa_prime * kappa_prime * tau;
     for (int d = 1; d <= D; ++d)

@@ -7,6 +7,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -76,10 +77,21 @@ void validate_tf(const sphray_tf_point* tf, size_t ntf);  // TransferFunction::v
 
 // io.cpp: io.hpp:62-216 restated
 std::vector<sphray_particle> load_particles(const std::string& path);
+bool is_sprt(const std::string& path);
+size_t read_sprt_into(const std::string& path, const std::function<sphray_particle*(size_t)>& alloc);
 void save_particles(const sphray_particle* ps, size_t n, const std::string& path, bool binary);
 std::vector<sphray_tf_point> load_transfer_function(const std::string& path);
 void save_ppm(const double* rgb, int W, int H, const std::string& path);
 sphray_camera load_camera(const std::string& path);
+std::vector<uint8_t> serialize_lut(const sphray_lut_view& v, const std::string& kernel_id);
+std::string render_report_json(const sphray_lut_view* lut, const std::string& kernel_id,
+                               const sphray_dataset_stats* ds, const sphray_quanta* qc,
+                               const sphray_render_stats* st, uint64_t seed, const std::string& image,
+                               double kappa, double kappa_prime);
+// overall_error (lut.hpp:284-290) and quantization_error (quantize.hpp:64-73)
+double overall_error(const LutHost& L, double kappa);
+double quantization_error(const LutHost& L, double kappa, double kappa_prime, double tau_rel,
+                          double sigma_rel);
 
 // probe.cu: measured issue peaks (int64 mul/add ops/s, fp64 flops/s) of this GPU
 void probe_alu_peaks(int device, double* int64_gops, double* fp64_gflops);

@@ -8,7 +8,9 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <cstdio>
 #include <fstream>
+#include <functional>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -65,32 +67,58 @@ constexpr const char* kCsvHeader = "x,y,z,mass,density,h,value";  // io.hpp:72
 
 }  // namespace
 
-std::vector<sphray_particle> load_particles(const std::string& path) {
+// read_particles_binary (io.hpp:118-138) straight into caller storage:
+// `alloc(n)` returns room for n records (e.g. pinned host memory, so the
+// upload is a true DMA), filled record by record from the file and validated
+// in the reference's order (a bad record before the truncation point is
+// reported first).  Returns the record count.
+size_t read_sprt_into(const std::string& path, const std::function<sphray_particle*(size_t)>& alloc) {
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) fail(SPHRAY_ERR_IO, "cannot open particle file " + path);
+    struct Closer {
+        std::FILE* f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    unsigned char head[12];
+    const size_t got = std::fread(head, 1, 12, f);
+    if (got < 4 || std::memcmp(head, "SPRT", 4) != 0) fail(SPHRAY_ERR_IO, path + ": bad magic");
+    if (got < 12) fail(SPHRAY_ERR_IO, "truncated file");
+    const uint64_t n = le64(head + 4);
+    std::fseek(f, 0, SEEK_END);
+    const long long size = std::ftell(f);
+    std::fseek(f, 12, SEEK_SET);
+    const uint64_t avail = size > 12 ? static_cast<uint64_t>(size - 12) / 56 : 0;
+    const uint64_t take = std::min(n, avail);
+    sphray_particle* out = alloc(static_cast<size_t>(take));
+    static_assert(sizeof(sphray_particle) == 56, "SPRT record layout");
+    // record fields are read with lut.hpp's detail::get_f64 (io.hpp declares
+    // only get_u64), whose truncation message is "lut: truncated file"
+    if (take && std::fread(out, 56, take, f) != take) fail(SPHRAY_ERR_IO, "lut: truncated file");
+    for (uint64_t i = 0; i < take; ++i)  // little-endian host: the record bytes are the doubles
+        check_particle(out[i], path + ": record " + std::to_string(i));
+    if (take < n) fail(SPHRAY_ERR_IO, "lut: truncated file");
+    return static_cast<size_t>(n);
+}
+
+bool is_sprt(const std::string& path) {
     std::ifstream f(path, std::ios::binary);
     if (!f) fail(SPHRAY_ERR_IO, "cannot open particle file " + path);
     char magic[4] = {};
     f.read(magic, 4);
-    f.clear();
-    f.seekg(0);
+    return f.gcount() == 4 && std::memcmp(magic, "SPRT", 4) == 0;
+}
+
+std::vector<sphray_particle> load_particles(const std::string& path) {
     std::vector<sphray_particle> out;
-    if (std::memcmp(magic, "SPRT", 4) == 0) {  // read_particles_binary, io.hpp:118-138
-        std::vector<unsigned char> buf((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
-        if (buf.size() < 12) fail(SPHRAY_ERR_IO, "truncated file");
-        const uint64_t n = le64(buf.data() + 4);
-        if ((buf.size() - 12) / 56 < n) fail(SPHRAY_ERR_IO, "lut: truncated file");
-        out.resize(n);
-        for (uint64_t i = 0; i < n; ++i) {
-            double v[7];
-            for (int k = 0; k < 7; ++k) {
-                const uint64_t bits = le64(buf.data() + 12 + i * 56 + k * 8);
-                std::memcpy(&v[k], &bits, 8);
-            }
-            sphray_particle& p = out[i];
-            p = sphray_particle{v[0], v[1], v[2], v[3], v[4], v[5], v[6]};
-            check_particle(p, path + ": record " + std::to_string(i));
-        }
+    if (is_sprt(path)) {
+        read_sprt_into(path, [&](size_t n) {
+            out.resize(n);
+            return out.data();
+        });
         return out;
     }
+    std::ifstream f(path, std::ios::binary);
+    if (!f) fail(SPHRAY_ERR_IO, "cannot open particle file " + path);
     // read_particles_csv, io.hpp:74-99
     std::string line;
     if (!std::getline(f, line)) fail(SPHRAY_ERR_IO, path + ": empty file");
@@ -229,6 +257,89 @@ sphray_camera load_camera(const std::string& path) {
     return c;
 #else
     fail(SPHRAY_ERR_IO, "camera json: library built without nlohmann/json (" + path + ")");
+#endif
+}
+
+// serialize_lut (lut.hpp:335-352): "SPLT", u32 version 1, 16-byte zero-padded
+// kernel id, f64 q, u32 K, D, N, then the N records as the view holds them
+// (f64 lambda, error, ceil(K/2) knots, floor(K*D/2) jumps), all little-endian.
+std::vector<uint8_t> serialize_lut(const sphray_lut_view& v, const std::string& kernel_id) {
+    const LutHost L = make_lut(v);  // validates K, D, N, q and the record order like deserialize_lut
+    const size_t per = 2 + static_cast<size_t>(L.m) + static_cast<size_t>(L.nj);
+    std::vector<uint8_t> out;
+    out.reserve(44 + static_cast<size_t>(L.N) * per * 8);
+    auto put = [&](const void* p, size_t n) {
+        const auto* b = static_cast<const uint8_t*>(p);
+        out.insert(out.end(), b, b + n);
+    };
+    auto u32 = [&](uint32_t x) {
+        uint8_t b[4];
+        for (int i = 0; i < 4; ++i) b[i] = static_cast<uint8_t>(x >> (8 * i));
+        put(b, 4);
+    };
+    auto f64 = [&](double d) {
+        uint64_t x;
+        std::memcpy(&x, &d, 8);
+        uint8_t b[8];
+        for (int i = 0; i < 8; ++i) b[i] = static_cast<uint8_t>(x >> (8 * i));
+        put(b, 8);
+    };
+    put("SPLT", 4);
+    u32(1);
+    char id[16] = {};
+    std::memcpy(id, kernel_id.data(), std::min<size_t>(kernel_id.size(), 16));
+    put(id, 16);
+    f64(v.q);
+    u32(static_cast<uint32_t>(v.K));
+    u32(static_cast<uint32_t>(v.D));
+    u32(static_cast<uint32_t>(v.N));
+    for (size_t i = 0; i < static_cast<size_t>(v.N) * per; ++i) f64(v.records[i]);
+    return out;
+}
+
+// The `render` report of the reference CLI (sphray_main.cpp:196-256): quanta,
+// RenderStats, dataset statistics, the approximation / quantization errors
+// (overall_error lut.hpp:284-290, quantization_error quantize.hpp:64-73) and
+// run metadata, as nlohmann::json::dump(2) text (the reference's writer).
+std::string render_report_json(const sphray_lut_view* lutv, const std::string& kernel_id,
+                               const sphray_dataset_stats* ds, const sphray_quanta* qc,
+                               const sphray_render_stats* st, uint64_t seed, const std::string& image,
+                               double kappa, double kappa_prime) {
+#if SPHRAY_HAVE_JSON
+    nlohmann::json report;
+    if (!lutv || !ds || !qc || !st || st->particles == 0) {
+        report["quanta"] = nullptr;
+        report["stats"] = {{"particles", 0}, {"knots", 0}, {"rays_touched", 0}};
+        report["errors"] = nullptr;
+        report["overflow_count"] = 0;
+    } else {
+        const LutHost L = make_lut(*lutv);
+        const double estar = overall_error(L, kappa);
+        const double qd = quantization_error(L, kappa, kappa_prime, qc->tau / ds->h_r, qc->sigma / ds->phi_repr);
+        report["quanta"] = {{"tau", qc->tau}, {"sigma", qc->sigma}, {"int_width", qc->int_width}};
+        report["stats"] = {{"particles", st->particles},
+                           {"skipped_particles", st->skipped_particles},
+                           {"knots", st->knots},
+                           {"rays_touched", st->rays_touched},
+                           {"int_ops", st->int_ops},
+                           {"residual_failures", st->residual_failures},
+                           {"step", st->step}};
+        report["dataset"] = {{"count", ds->count},
+                             {"h_r", ds->h_r},
+                             {"phi_repr", ds->phi_repr},
+                             {"a_max", ds->a_max},
+                             {"clustering_factor", ds->clustering_factor}};
+        report["errors"] = {{"E_star", estar}, {"Q_D", qd}, {"combined", std::hypot(estar, qd)}};
+        report["overflow_count"] = 0;  // an overflow aborts the run instead
+        report["K"] = L.K;
+        report["D"] = L.D;
+    }
+    report["kernel"] = kernel_id;
+    report["seed"] = seed;
+    report["image"] = image;
+    return report.dump(2) + "\n";
+#else
+    fail(SPHRAY_ERR_CONFIG, "built without nlohmann/json: no render report");
 #endif
 }
 

@@ -39,10 +39,13 @@ struct HitPositions {
 // Phase A.  Returns false when quantize_particle emits nothing (lam >= q,
 // quantize.hpp:204).  All array indices are compile-time (M and the parity of
 // K are template parameters) so nothing spills to local memory.
-template <int M, bool EVEN>
+// N32: the kernel variant that serves int_width 32 (Q.w32 at run time):
+// every Checked value also has to fit int32 (narrow32).
+template <int M, bool EVEN, bool N32 = false>
 __device__ __forceinline__ bool quantize_positions(const QuantParams& Q, double h, double lam,
                                                    double tchi, HitPositions<M>& hp,
                                                    bool& ovf) {
+    const bool n32 = N32 && Q.w32;
     constexpr int KN = HitPositions<M>::KN;
     constexpr bool even = EVEN;  // K even (compile time: dead closure code stays out)
     hp.nraw = even ? KN : KN - 1;
@@ -54,14 +57,16 @@ __device__ __forceinline__ bool quantize_positions(const QuantParams& Q, double 
     if (!(lam < Q.q)) return false;
     const int e = lut_index(lam, Q.lut_dl, Q.inv_dl, Q.lut_N);
     hp.row = Q.lut_rows + static_cast<size_t>(e) * Q.lut_stride;
-    hp.pos[0] = rint_div(tchi, Q.tau, Q.inv_tau, ovf);
+    hp.pos[0] = narrow32(rint_div(tchi, Q.tau, Q.inv_tau, ovf), n32, ovf);
 #pragma unroll
     for (int k = 1; k <= M; ++k)
-        hp.pos[k] = cadd(hp.pos[0], rint_div(dmul(h, hp.row[k - 1]), Q.tau, Q.inv_tau, ovf), ovf);
-    const int64_t twice = cadd(hp.pos[0], hp.pos[0], ovf);
+        hp.pos[k] = narrow32(
+            cadd(hp.pos[0], narrow32(rint_div(dmul(h, hp.row[k - 1]), Q.tau, Q.inv_tau, ovf), n32, ovf), ovf),
+            n32, ovf);
+    const int64_t twice = narrow32(cadd(hp.pos[0], hp.pos[0], ovf), n32, ovf);
     bool ov2 = false;  // the negative side is evaluated for all k; flags count once
 #pragma unroll
-    for (int i = 0; i < M; ++i) hp.kpos[i] = csub(twice, hp.pos[M - i], ov2);  // lut.hpp:150
+    for (int i = 0; i < M; ++i) hp.kpos[i] = narrow32(csub(twice, hp.pos[M - i], ov2), n32, ov2);  // lut.hpp:150
     ovf |= ov2;
     // positive side (lut.hpp:154-166): even K puts the centre at index m
 #pragma unroll
@@ -81,10 +86,12 @@ __device__ __forceinline__ bool quantize_positions(const QuantParams& Q, double 
 // (quantize.hpp:221-222 with the libm parts precomputed on the host),
 // X[2D..3D) = recip_or_nan(X[D..2D)) for rint_div.
 // sink(o, t, b) receives distinct knot o (0..nk) with its D+1 jumps.
-template <int D, int M, bool EVEN, class Sink>
+template <int D, int M, bool EVEN, class Sink, bool N32 = false>
 __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double* X,
                                               const HitPositions<M>& hp, bool& ovf,
                                               Sink&& sink) {
+    const bool n32 = N32 && Q.w32;
+    auto nw = [&](int64_t v) { return narrow32(v, n32, ovf); };
     constexpr int m = M;
     constexpr int KN = HitPositions<M>::KN;
     constexpr bool even = EVEN;  // K even (compile time: dead closure code stays out)
@@ -108,8 +115,8 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
             } else {
                 ii = c1 + (k - 2) * D + (d - 1);
             }
-            const int64_t bp = rint_div(dmul(X[d - 1], hp.row[m + ii]), X[D + d - 1], X[2 * D + d - 1], ovf);
-            negk[k - 1][d] = (d & 1) ? bp : cneg(bp, ovf);  // lut.hpp:107-109
+            const int64_t bp = nw(rint_div(dmul(X[d - 1], hp.row[m + ii]), X[D + d - 1], X[2 * D + d - 1], ovf));
+            negk[k - 1][d] = (d & 1) ? bp : nw(cneg(bp, ovf));  // lut.hpp:107-109
         }
     }
     if (even) {
@@ -119,17 +126,17 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
             int64_t acc = 0;
 #pragma unroll
             for (int k = 1; k <= M; ++k) {
-                const int64_t off = csub(hp.pos[k], hp.pos[0], ovf);
+                const int64_t off = nw(csub(hp.pos[k], hp.pos[0], ovf));
                 int64_t pw = 1;  // off^(j-d), built one step at a time as lut.hpp:123-126
 #pragma unroll
                 for (int j = d; j <= D; ++j) {
-                    int64_t t = cmul_binom(negk[k - 1][j], binom(j, d), ovf);
-                    if (j > d) t = cmul(t, pw, ovf);  // * 1 at j == d
-                    acc = cadd(acc, t, ovf);
-                    if (j < D) pw = (j == d) ? off : cmul(pw, off, ovf);
+                    int64_t t = nw(cmul_binom(negk[k - 1][j], binom(j, d), ovf));
+                    if (j > d) t = nw(cmul(t, pw, ovf));  // * 1 at j == d
+                    acc = nw(cadd(acc, t, ovf));
+                    if (j < D) pw = (j == d) ? off : nw(cmul(pw, off, ovf));
                 }
             }
-            center[d] = cneg(cadd(acc, acc, ovf), ovf);
+            center[d] = nw(cneg(nw(cadd(acc, acc, ovf)), ovf));
         }
     } else {
         // odd K: the innermost pair closes, descending odd d (lut.hpp:131-145)
@@ -137,18 +144,18 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
         for (int d = (D % 2 == 1 ? D : D - 1); d >= 1; d -= 2) {
             int64_t acc = 0;
 #pragma unroll
-            for (int k = 2; k <= M; ++k) acc = cadd(acc, negk[k - 1][d], ovf);
+            for (int k = 2; k <= M; ++k) acc = nw(cadd(acc, negk[k - 1][d], ovf));
 #pragma unroll
             for (int k = 1; k <= M; ++k) {
-                const int64_t off = csub(hp.pos[k], hp.pos[0], ovf);
+                const int64_t off = nw(csub(hp.pos[k], hp.pos[0], ovf));
                 int64_t pw = off;
 #pragma unroll
                 for (int j = d + 1; j <= D; ++j) {
-                    acc = cadd(acc, cmul(cmul_binom(negk[k - 1][j], binom(j, d), ovf), pw, ovf), ovf);
-                    if (j < D) pw = cmul(pw, off, ovf);
+                    acc = nw(cadd(acc, nw(cmul(nw(cmul_binom(negk[k - 1][j], binom(j, d), ovf)), pw, ovf)), ovf));
+                    if (j < D) pw = nw(cmul(pw, off, ovf));
                 }
             }
-            negk[0][d] = cneg(acc, ovf);
+            negk[0][d] = nw(cneg(acc, ovf));
         }
     }
     // jumps in emission order (lut.hpp:147-166), static indices like kpos
@@ -168,7 +175,8 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
 #pragma unroll
     for (int k = 1; k <= M; ++k)
 #pragma unroll
-        for (int d = 0; d <= D; d += 2) ovf |= negk[k - 1][d] == INT64_MIN;
+        for (int d = 0; d <= D; d += 2)
+            ovf |= negk[k - 1][d] == INT64_MIN || (n32 && negk[k - 1][d] == INT32_MIN);
     // coincident merge of quantize.hpp:229-242
     int64_t cur[D + 1];
 #pragma unroll
@@ -179,7 +187,7 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
         if (q < hp.nraw) {
             if (hp.kpos[q] == hp.kpos[q - 1]) {
 #pragma unroll
-                for (int d = 0; d <= D; ++d) cur[d] = cadd(cur[d], jump(q, d), ovf);
+                for (int d = 0; d <= D; ++d) cur[d] = nw(cadd(cur[d], jump(q, d), ovf));
             } else {
                 sink(o++, hp.kpos[q - 1], cur);
 #pragma unroll

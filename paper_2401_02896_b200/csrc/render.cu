@@ -120,6 +120,22 @@ __global__ void k_tile_ranges(const uint32_t* keys, size_t m, uint32_t* begin, u
     if (i == m - 1 || keys[i + 1] != t) end[t] = static_cast<uint32_t>(i + 1);
 }
 
+__global__ void k_records(const uint32_t* tile_keys, const uint32_t* cand, size_t m, const double4* pxyzh,
+                          const int4* bbox, const float* front, int tiles_x, int rank, int nranks,
+                          double4* cxyzh, uint4* cmeta) {
+    const size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const uint32_t i = cand[j];
+    const uint32_t local = tile_keys[j];
+    const uint32_t tile = nranks > 1 ? local * nranks + rank : local;
+    const int tx0 = static_cast<int>(tile % tiles_x) * kTile, ty0 = static_cast<int>(tile / tiles_x) * kTile;
+    const int4 b = bbox[i];
+    const uint32_t x0 = max(b.x - tx0, 0), x1 = min(b.y - tx0, kTile - 1);
+    const uint32_t y0 = max(b.z - ty0, 0), y1 = min(b.w - ty0, kTile - 1);
+    cxyzh[j] = pxyzh[i];
+    cmeta[j] = make_uint4(__float_as_uint(front[i]), i, x0 | (x1 << 4) | (y0 << 8) | (y1 << 12), 0u);
+}
+
 // skipped_particles (raycast.hpp:437-438, 452): particles with an empty footprint.
 __global__ void k_reach(const CamConst cam, int n, double q, const double4* pxyzh,
                         const int4* bbox, unsigned long long* skipped) {
@@ -358,6 +374,15 @@ void launch_emit(const PrepParams& p, const uint32_t* order, const uint32_t* off
 void launch_tile_ranges(const uint32_t* keys, size_t m, uint32_t* begin, uint32_t* end, cudaStream_t s) {
     if (m == 0) return;
     k_tile_ranges<<<grid_for(m, 256), 256, 0, s>>>(keys, m, begin, end);
+    SPHRAY_CUDA_OK(cudaGetLastError());
+}
+
+void launch_records(const uint32_t* tile_keys, const uint32_t* cand, size_t m, const double4* pxyzh,
+                    const int4* bbox, const float* front, int tiles_x, int rank, int nranks,
+                    double4* cxyzh, uint4* cmeta, cudaStream_t s) {
+    if (m == 0) return;
+    k_records<<<grid_for(m, 256), 256, 0, s>>>(tile_keys, cand, m, pxyzh, bbox, front, tiles_x, rank, nranks,
+                                              cxyzh, cmeta);
     SPHRAY_CUDA_OK(cudaGetLastError());
 }
 

@@ -46,6 +46,7 @@ struct QuantParams {
     int K, m;
     double tau, sigma;
     double inv_tau, inv_dl;  // recip_or_nan(tau), recip_or_nan(lut_dl): division fast paths
+    int w32;                 // int_width 32: every checked value must fit int32 (robust variant)
 };
 
 // Per-frame constants of the render kernel.
@@ -59,8 +60,9 @@ struct FrameParams {
     const int4* bbox;      // reference footprint bbox per particle (clipped)
     const float* front;    // knot-position lower bound (world units, rounded down)
     const int32_t* orig;   // original particle index
-    // binning
-    const uint32_t* cand;        // particle indices, sorted by (tile, front)
+    // binning: the candidate records of every owned tile, in front order
+    const double4* cxyzh;        // x, y, z, h of the candidate
+    const uint4* cmeta;          // front (float bits), particle index, tile-local bbox (4 x 4 bits), 0
     const uint32_t* tile_begin;  // per owned tile
     const uint32_t* tile_end;
     int tiles_x, tiles_y;
@@ -182,6 +184,11 @@ void launch_gather_counts(const uint32_t* counts, const uint32_t* order, int n, 
 void launch_emit(const PrepParams& p, const uint32_t* order, const uint32_t* offsets, uint32_t* keys,
                  uint32_t* vals, cudaStream_t s);
 void launch_tile_ranges(const uint32_t* keys, size_t m, uint32_t* begin, uint32_t* end, cudaStream_t s);
+// candidate records in sorted (tile, front) order: the particle's x, y, z, h and
+// (front, index, its reference bbox clipped to the tile in tile-local pixels)
+void launch_records(const uint32_t* tile_keys, const uint32_t* cand, size_t m, const double4* pxyzh,
+                    const int4* bbox, const float* front, int tiles_x, int rank, int nranks,
+                    double4* cxyzh, uint4* cmeta, cudaStream_t s);
 void launch_reach(const CamConst& cam, int n, double q, const double4* pxyzh, const int4* bbox,
                   unsigned long long* skipped, cudaStream_t s);
 void launch_unpack(const double* packed, size_t per_rank, int nranks, int tiles_x, int W, int H,

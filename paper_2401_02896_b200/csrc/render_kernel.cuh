@@ -143,7 +143,33 @@ __device__ __forceinline__ int sample_count(double len, double step, double inv_
 // 1 - exp(-x) as the reference writes it (CUDA's exp is within 1 ulp of
 // glibc's).  Either way alpha is within a few ulps of the reference's, so the
 // early-termination test T <= 1e-3 sees the same transmittance to ~1e-15.
+#ifndef SPHRAY_ALPHA_MODE
+#define SPHRAY_ALPHA_MODE 0  // diagnostics: 1 = round-1 fp32 alpha (4-term series, __expf)
+#endif
+#ifndef SPHRAY_OVF_CHECK
+#define SPHRAY_OVF_CHECK 2  // genuine-overflow test of the merge: 2 fp32 high words (fp64 for long steps), 1 fp64, 0 off (diagnostics)
+#endif
+#ifndef SPHRAY_RECORDS
+#define SPHRAY_RECORDS 1  // diagnostics: 0 = no per-ray piece checksum code in the walk
+#endif
 __device__ __forceinline__ double alpha_of(double x) {
+    if (SPHRAY_ALPHA_MODE == 1) {
+        if (x < 0.05) return x * (1.0 - x * (0.5 - x * (1.0 / 6.0 - x * (1.0 / 24.0))));
+        return 1.0 - static_cast<double>(__expf(-static_cast<float>(x)));
+    }
+    if (SPHRAY_ALPHA_MODE == 2) {  // series to x^6 below 1/16 (relative error < 7e-13)
+        if (x < 0.0625) {
+            double s = 1.0 / 5040.0;
+            s = fma(s, -x, 1.0 / 720.0);
+            s = fma(s, -x, 1.0 / 120.0);
+            s = fma(s, -x, 1.0 / 24.0);
+            s = fma(s, -x, 1.0 / 6.0);
+            s = fma(s, -x, 0.5);
+            s = fma(s, -x, 1.0);
+            return s * x;
+        }
+        return 1.0 - exp(-x);
+    }
     if (x < 0.0625) {
         double s = 1.0 / 40320.0;
         s = fma(s, -x, 1.0 / 5040.0);
@@ -186,6 +212,7 @@ __device__ __forceinline__ uint64_t piece_mix(int64_t t, const uint64_t (&a)[D +
 template <int D>
 __device__ __forceinline__ bool shift_overflows(const double (&v)[D + 1], double delta,
                                                 const uint64_t (&w)[D + 1]) {
+    if (!SPHRAY_OVF_CHECK) return false;
     double p[D + 1];
 #pragma unroll
     for (int d = 0; d <= D; ++d) p[d] = v[d];
@@ -200,10 +227,41 @@ __device__ __forceinline__ bool shift_overflows(const double (&v)[D + 1], double
     return bad;
 }
 
+// The same test for one walk step, from the wrapped coefficients before (b)
+// and after (a) the shift.  Steps of fewer than 256 quanta (the common case)
+// run it in fp32 on the high 32-bit words (units of 2^32): truncating the low
+// words costs < 1 unit, amplified at most (1 + delta)^D < 2^24 units by the
+// shift, far below the 2^30-unit (2^62) threshold an overflow (a difference
+// of k 2^32 units) must cross; longer steps take the fp64 form.
+template <int D>
+__device__ __forceinline__ bool step_overflows(const uint64_t (&b)[D + 1], uint64_t dl,
+                                               const uint64_t (&a)[D + 1]) {
+    if (!SPHRAY_OVF_CHECK) return false;
+    if (SPHRAY_OVF_CHECK == 2 && dl < 256) {
+        float p[D + 1];
+#pragma unroll
+        for (int d = 0; d <= D; ++d) p[d] = static_cast<float>(static_cast<int32_t>(b[d] >> 32));
+        const float dd = static_cast<float>(static_cast<uint32_t>(dl));
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = D - 1; j >= i; --j) p[j] = fmaf(dd, p[j + 1], p[j]);
+        bool bad = false;
+#pragma unroll
+        for (int d = 0; d < D; ++d)  // a_D is unchanged by a shift
+            bad |= !(fabsf(p[d] - static_cast<float>(static_cast<int32_t>(a[d] >> 32))) < 0x1p30f);
+        return bad;
+    }
+    double v[D + 1];
+#pragma unroll
+    for (int d = 0; d <= D; ++d) v[d] = static_cast<double>(static_cast<int64_t>(b[d]));
+    return shift_overflows<D>(v, static_cast<double>(static_cast<int64_t>(dl)), a);
+}
+
 // a += j modulo 2^64, flagging signed overflow (Checked<int64_t> +, int_ops.hpp:73-80)
 __device__ __forceinline__ uint64_t add_checked(uint64_t a, uint64_t j, bool& o) {
     const uint64_t r = a + j;
-    o |= static_cast<int64_t>((a ^ r) & (j ^ r)) < 0;
+    if (SPHRAY_OVF_CHECK) o |= static_cast<int64_t>((a ^ r) & (j ^ r)) < 0;
     return r;
 }
 
@@ -467,20 +525,26 @@ class RayWorker {
             const int64_t t = tn;
             if (t != tcur) {
                 const uint64_t dl = static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur);
-                double v[D + 1];
+                uint64_t before[D + 1];
 #pragma unroll
-                for (int d = 0; d <= D; ++d) v[d] = static_cast<double>(static_cast<int64_t>(Pc[d]));
+                for (int d = 0; d <= D; ++d) before[d] = Pc[d];
                 taylor_shift<D>(Pc, dl);
-                aovf |= shift_overflows<D>(v, static_cast<double>(static_cast<int64_t>(dl)), Pc);
+                aovf |= step_overflows<D>(before, dl, Pc);
                 tcur = t;
             }
 #pragma unroll
-            for (int d = 1; d <= D; ++d) Pc[d] = add_checked(Pc[d], pool_c(d, s), aovf);
+            for (int d = 1; d <= D; ++d) {
+                Pc[d] = add_checked(Pc[d], pool_c(d, s), aovf);
+                if constexpr (DUMP) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
+            }
             const bool more = k + 1 < nsel;
             tn = more ? pool_t(fs[k + 1]) : t;
             if (more && tn == t) continue;  // more jumps at this position
             ++npc;
-            if (P.ray_rec && !stop) csum += piece_mix<D>(t, Pc);
+            if constexpr (DUMP)
+#pragma unroll
+                for (int d = 0; d <= D; ++d) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
+            if (SPHRAY_RECORDS && P.ray_rec && !stop) csum += piece_mix<D>(t, Pc);
             if constexpr (DUMP)
                 if (!stop && P.dump_piece_t) dump_piece(t, Pc);
             if (!more) {
@@ -799,7 +863,7 @@ class RayWorker {
         }
         bool ovf = false;
         HitPositions<M> hp;
-        bool emits = act && quantize_positions<M, EVEN>(P.Q, h, lam, tchi, hp, ovf);
+        bool emits = act && quantize_positions<M, EVEN, DUMP>(P.Q, h, lam, tchi, hp, ovf);
         int nk = emits ? hp.nk : 0;
         if (ovf) {
             report_overflow(pi);
@@ -823,7 +887,7 @@ class RayWorker {
             const double* xs = P.xy + static_cast<size_t>(pi) * (3 * D);
 #pragma unroll
             for (int d = 0; d < 3 * D; ++d) X[d] = xs[d];
-            quantize_emit<D, M, EVEN>(P.Q, X, hp, ovf, [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
+            auto sink = [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
                 const int slot = w.fl[slot0 + o];
                 // b[0] is structurally zero (lut.hpp:107-166): only orders 1..D are stored
                 const uint64_t to = static_cast<uint64_t>(t) - static_cast<uint64_t>(tb);
@@ -832,7 +896,8 @@ class RayWorker {
 #pragma unroll
                 for (int d = 1; d <= D; ++d) pool_c(d, slot) = static_cast<uint64_t>(b[d]);
                 w.ps[np + off + o] = static_cast<uint16_t>(slot);
-            });
+            };
+            quantize_emit<D, M, EVEN, decltype(sink)&, DUMP>(P.Q, X, hp, ovf, sink);
             if (ovf) report_overflow(pi);
         }
         // a ray spanning more than 2^32 position quanta does not fit the
@@ -877,6 +942,7 @@ class RayWorker {
         const int tile = (py >> kTileShift) * P.tiles_x + (px >> kTileShift);
         const int local = P.nranks > 1 ? tile / P.nranks : tile;
         const uint32_t cb = P.tile_begin[local], ce = P.tile_end[local];
+        const uint32_t lx = static_cast<uint32_t>(px & (kTile - 1)), ly = static_cast<uint32_t>(py & (kTile - 1));
         const double near_plane = P.cam.near_plane, far_plane = P.cam.far_plane;
         uint32_t cursor = cb;
         int hq_n = 0;
@@ -889,13 +955,15 @@ class RayWorker {
                 double d2 = 0.0, tchi = 0.0;
                 uint32_t pi = 0;
                 if (c < ce) {
-                    pi = P.cand[c];
-                    const int4 bb = P.bbox[pi];
-                    if (px >= bb.x && px <= bb.y && py >= bb.z && py <= bb.w) {
-                        const double4 p = P.pxyzh[pi];
+                    // the tile's candidate record (coalesced: consecutive lanes read
+                    // consecutive records, both loads issued together)
+                    const uint4 mt = P.cmeta[c];
+                    const double4 p = P.cxyzh[c];
+                    pi = mt.y;
+                    if (lx >= (mt.z & 15u) && lx <= ((mt.z >> 4) & 15u) && ly >= ((mt.z >> 8) & 15u) &&
+                        ly <= ((mt.z >> 12) & 15u))
                         hit = hit_test(ray, p.x, p.y, p.z, dmul(P.Q.q, p.w), near_plane, far_plane,
                                        d2, tchi);
-                    }
                 }
                 const unsigned m = __ballot_sync(kFull, hit);
                 if (hit) {
@@ -958,8 +1026,8 @@ class RayWorker {
             const bool final_ = hq_n == 0 && cursor >= ce;
             int64_t F = INT64_MAX;
             if (!final_) {
-                const uint32_t pn = hq_n > 0 ? static_cast<uint32_t>(w.hq_p[0]) : P.cand[cursor];
-                F = knot_floor(P.front[pn], P.inv_tau);
+                const float fr = hq_n > 0 ? P.front[w.hq_p[0]] : __uint_as_float(P.cmeta[cursor].x);
+                F = knot_floor(fr, P.inv_tau);
             }
             if (final_ || stuck || nfree < 32 * KN || np >= (P.cap * SPHRAY_FLUSH_AT) / 8) {
                 const int np0 = np;
@@ -1097,7 +1165,7 @@ __global__ void k_quantize_hits(const QuantParams Q, const sphray_particle* ps, 
     const sphray_particle p = ps[i];
     bool ovf = false;
     HitPositions<M> hp;
-    if (!quantize_positions<M, EVEN>(Q, p.h, lam[i], tchi[i], hp, ovf)) {
+    if (!quantize_positions<M, EVEN, true>(Q, p.h, lam[i], tchi[i], hp, ovf)) {
         knot_count[i] = ovf ? -1 : 0;
         return;
     }
@@ -1108,12 +1176,13 @@ __global__ void k_quantize_hits(const QuantParams Q, const sphray_particle* ps, 
         X[2 * D + d - 1] = recip_or_nan(X[D + d - 1]);
     }
     const int stride = Q.K + 1;
-    quantize_emit<D, M, EVEN>(Q, X, hp, ovf, [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
+    auto sink = [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
         if (o < KN && o < stride) {
             knot_t[i * stride + o] = t;
             for (int d = 0; d <= D; ++d) knot_b[(i * stride + o) * (D + 1) + d] = b[d];
         }
-    });
+    };
+    quantize_emit<D, M, EVEN, decltype(sink)&, true>(Q, X, hp, ovf, sink);
     knot_count[i] = ovf ? -1 : hp.nk;
 }
 

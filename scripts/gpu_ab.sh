@@ -9,7 +9,7 @@ for rep in $(seq 1 $REPS); do
   for v in "${VS[@]}"; do
     IFS='|' read -r name lib args envs <<< "$v"
     if [ "$lib" = "-" ]; then unset SPHRAY_B200_LIB; else export SPHRAY_B200_LIB=$PWD/$lib; fi
-    timeout 900 env SPHRAY_TRACE=1 $envs python bench.py --config $CFG --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 $args \
+    timeout 900 env SPHRAY_TRACE=1 $envs python bench.py --config $CFG --steps 3 --warmup 3 --no-parity --exact-steps 0 --e2e-steps 0 $args \
       > gpurun_out/ab_${name}_${rep}.json 2> gpurun_out/ab_${name}_${rep}.err
     python - "$name" "$rep" <<'PY' >> gpurun_out/ab_summary.txt
 import json,sys

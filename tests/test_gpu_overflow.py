@@ -105,7 +105,7 @@ def test_spurious_reference_overflow_is_not_reproduced(ctx):
         ref.render(ps, ref.Camera(**CAM), H.SYNTH_TF, rl, rqc, rds, threads=1)
     assert er.value.code == 3
     assert not bad_rays(ps, rl, rqc)
-    rgb, rst, _, _ = ref.render(ps, ref.Camera(**CAM), H.SYNTH_TF, rl, rqc, rds, accum_bits=128)
+    rgb, rst, _ = ref.render(ps, ref.Camera(**CAM), H.SYNTH_TF, rl, rqc, rds, accum_bits=128)
     img, st = S.render_scene(ps, S.Camera(**CAM), S.TransferFunction.from_array(H.SYNTH_TF), lut,
                              qc, ds, S.RenderOptions(mode=S.MODE_EXACT), ctx=ctx)
     assert np.abs(img.pixels - rgb).max() <= 1e-4
@@ -132,3 +132,70 @@ def test_quantize_overflow_names_particle_and_ray(ctx):
                        ctx=ctx)
     assert e.value.particle_index == 7
     assert "particle 7" in str(e.value)
+
+
+# --------------------------------------------------------------------------- int_width 32
+# render_scene<int32_t> (dispatch_int_width, int_ops.hpp:113-121): every
+# Checked<int32_t> value of quantize_particle and every merged coefficient must
+# fit int32; the GPU computes in int64 and tests the int32 range of each.
+
+@pytest.mark.parametrize("case", ["render_test", "blob", "render_test_K2D1"])
+def test_int32_renders_match_reference(ctx, case):
+    if case == "blob":
+        ps, ck, tf, lp = ref.generate_scene(1, 3000), H.synth_camera_kwargs(48, 48), H.SYNTH_TF, \
+            H.lut_path(4, 3, 1024)
+    else:
+        ps = H.random_cloud(H.MT19937_64(31337), 120, 1.6, -1.2, 1.2)
+        ck, tf = H.render_test_camera_kwargs(), H.TEST_TF
+        lp = H.lut_path(2, 1, 1024) if case.endswith("K2D1") else H.lut_path(4, 3, 16)
+    lut, rl = S.load_lut(lp), ref.Lut(lp)
+    ds = S.dataset_stats(ps, lut)
+    qc = S.choose_quanta(lut, ds, 32)
+    rds = ref.dataset_stats(ps, rl)
+    rqc = ref.choose_quanta(rl, rds, 32)
+    assert (qc.tau, qc.sigma, qc.width) == (rqc.tau, rqc.sigma, 32)
+    rgb, rst, _ = ref.render(ps, ref.Camera(**ck), tf, rl, rqc, rds, accum_bits=32)
+    img, st = S.render_scene(ps, S.Camera(**ck), S.TransferFunction.from_array(tf), lut, qc, ds,
+                             S.RenderOptions(mode=S.MODE_EXACT), ctx=ctx)
+    assert np.abs(img.pixels - rgb).max() <= 1e-4
+    for k in ("knots", "rays_touched", "int_ops", "residual_failures", "skipped_particles"):
+        assert getattr(st, k) == rst[k], k
+
+
+def test_int32_distant_particle_overflows_but_int64_renders(ctx, tmp_path):
+    """cli_tests.cpp:252-273: a particle 2e7 away overflows 32-bit knot
+    positions (OverflowError naming particle and ray, exit code 3 in the CLI)
+    but renders at 64 bits."""
+    small = np.array([[-0.8, 0.5, 0.3, 1.0, 1.2, 0.6, 1.5], [0.4, -0.6, -0.4, 0.8, 0.9, 0.8, 2.0],
+                      [0.9, 0.8, 0.8, 1.2, 1.1, 0.5, 0.7], [-0.3, -0.9, -0.9, 0.6, 1.0, 0.9, 1.1],
+                      [0.1, 0.2, 0.5, 1.5, 1.4, 0.7, 2.4], [-1.0, -0.2, 0.0, 0.9, 0.8, 0.6, 0.9],
+                      [0.0, 0.0, -2e7, 1.0, 1.0, 0.5, 1.0]])
+    ck = dict(mode="orthographic", position=(0.0, 0.0, 4.0), look_at=(0.0, 0.0, 0.0),
+              up=(0.0, 1.0, 0.0), width=16, height=16, ortho_height=4.0)
+    tf = np.array([[0.0, 0.0, 0.0, 0.0, 0.0], [1.0, 1.0, 0.5, 0.2, 2.0], [5.0, 1.0, 1.0, 1.0, 4.0]])
+    lp = str(tmp_path / "k2d1n8.splt")
+    ref.build_lut(2, 1, 8, lp)  # lut-build --K 2 --D 1 -N 8
+    lut, rl = S.load_lut(lp), ref.Lut(lp)
+    ds, rds = S.dataset_stats(small, lut), ref.dataset_stats(small, rl)
+    q32, r32 = S.choose_quanta(lut, ds, 32), ref.choose_quanta(rl, rds, 32)
+    with pytest.raises(ref.RefError) as er:
+        ref.render(small, ref.Camera(**ck), tf, rl, r32, rds, accum_bits=32)
+    with pytest.raises(S.OverflowError) as e:
+        S.render_scene(small, S.Camera(**ck), S.TransferFunction.from_array(tf), lut, q32, ds, ctx=ctx)
+    assert (e.value.particle_index, e.value.ray_id) == (er.value.particle_index, er.value.ray_id)
+    q64, r64 = S.choose_quanta(lut, ds, 64), ref.choose_quanta(rl, rds, 64)
+    rgb, rst, _ = ref.render(small, ref.Camera(**ck), tf, rl, r64, rds, accum_bits=64)
+    img, st = S.render_scene(small, S.Camera(**ck), S.TransferFunction.from_array(tf), lut, q64, ds,
+                             S.RenderOptions(mode=S.MODE_EXACT), ctx=ctx)
+    assert np.abs(img.pixels - rgb).max() <= 1e-4
+    for k in ("knots", "rays_touched", "int_ops", "residual_failures"):
+        assert getattr(st, k) == rst[k], k
+
+
+def test_int128_is_a_config_error(ctx):
+    ps = H.random_cloud(H.MT19937_64(31337), 20, 1.6, -1.2, 1.2)
+    lut = S.load_lut(H.lut_path(4, 3, 16))
+    ds = S.dataset_stats(ps, lut)
+    with pytest.raises(S.ConfigError):
+        S.render_scene(ps, S.Camera(**H.render_test_camera_kwargs()), S.TransferFunction.from_array(H.TEST_TF),
+                       lut, S.choose_quanta(lut, ds, 128), ds, ctx=ctx)

@@ -170,3 +170,68 @@ def test_camera_json_matches_reference(tmp_path, case):
         for k in ("mode", "position", "look_at", "up", "width", "height", "fov_deg",
                   "ortho_height", "near", "far"):
             assert getattr(va, k) == getattr(vb, k) or tuple(getattr(va, k)) == tuple(getattr(vb, k)), k
+
+
+def _msg_ours(fn, *a):
+    try:
+        fn(*a)
+        return "ok"
+    except (S.ConfigError, S.IoError) as e:
+        return str(e)
+
+
+def _msg_ref(fn, *a):
+    try:
+        fn(*a)
+        return "ok"
+    except ref.RefError as e:
+        return str(e).split(": ", 1)[1]
+
+
+def test_particle_binary_error_messages_match_reference(tmp_path):
+    """read_particles_binary (io.hpp:118-138): truncation reports 'truncated
+    file'; a bad record before the truncation point is reported first."""
+    ps = cloud(10)
+    path = str(tmp_path / "p.sprt")
+    S.save_particles(ps, path, binary=True)
+    raw = open(path, "rb").read()
+    bad = raw[:12 + 5 * 8] + np.float64(-1.0).tobytes() + raw[12 + 6 * 8:]
+    for name, data in [("truncated", raw[:-3]), ("bad_then_truncated", bad[:-3]),
+                       ("bad_magic", b"SPRX" + raw[4:])]:
+        p = str(tmp_path / (name + ".sprt"))
+        open(p, "wb").write(data)
+        assert _msg_ours(S.load_particles, p) == _msg_ref(ref.load_particles, p), name
+
+
+@pytest.mark.parametrize("name", sorted(os.listdir(H.LUTS)))
+def test_lut_serialize_is_the_reference_file(tmp_path, name):
+    """serialize_lut / save_lut (lut.hpp:335-352, 395-399): the committed tables
+    were written by the reference's save_lut; re-serialising gives the same bytes."""
+    path = os.path.join(H.LUTS, name)
+    lut = S.load_lut(path)
+    raw = open(path, "rb").read()
+    assert lut.serialize() == raw
+    out = str(tmp_path / name)
+    S.save_lut(lut, out)
+    assert open(out, "rb").read() == raw
+
+
+@pytest.mark.parametrize("width", [32, 64])
+def test_render_report_matches_reference_cli(width):
+    """The CLI's render report (sphray_main.cpp:196-256), field for field and
+    byte for byte, given the same RenderStats (here the reference's own)."""
+    ps = H.random_cloud(H.MT19937_64(31337), 120, 1.6, -1.2, 1.2)
+    ck = H.render_test_camera_kwargs()
+    lp = H.lut_path(4, 3, 16)
+    rl, lut = ref.Lut(lp), S.load_lut(lp)
+    want = ref.render_report(ps, ref.Camera(**ck), H.TEST_TF, rl, width, seed=5, image="out.ppm")
+    ds = S.dataset_stats(ps, lut)
+    qc = S.choose_quanta(lut, ds, width)
+    rds = ref.dataset_stats(ps, rl)
+    _, rst, _ = ref.render(ps, ref.Camera(**ck), H.TEST_TF, rl, ref.choose_quanta(rl, rds, width), rds,
+                           accum_bits=width)
+    got = S.render_report(lut, ds, qc, S.RenderStats(**rst), seed=5, image="out.ppm")
+    assert got == want
+    empty = ref.render_report(np.zeros((0, 7)), ref.Camera(**ck), H.TEST_TF, rl, width, seed=5,
+                              image="out.ppm")
+    assert S.render_report(lut, ds, qc, None, seed=5, image="out.ppm") == empty
