@@ -273,6 +273,21 @@ sphray_status sphray_scene_pieces(sphray_context* ctx, const sphray_camera* cam,
                                   size_t cap_rays, size_t cap_pieces, size_t* n_rays,
                                   size_t* n_pieces, sphray_error* err);
 
+/* accumulate<int64_t> (raycast.hpp:261-292) for explicit knot streams, one
+ * per ray, on the GPU (the render kernel's merge without the window): ray r's
+ * knots are [knot_offsets[r], knot_offsets[r+1]) of knot_t / knot_b, sorted by
+ * t, with 7 (max_degree + 1) jumps per knot in knot_b (QuantizedKnot::b).
+ * Output: one FieldPiece per distinct position as CSR -- piece_offsets
+ * (nrays + 1), piece_t, piece_a (D + 1 per piece); capacity = total knots
+ * suffices -- and per-ray RayAccumulator op counts (optional).  NumericError
+ * for unsorted knots (raycast.hpp:212-213); OverflowError naming the ray for a
+ * genuine int64 overflow of a coefficient (raycast.hpp:285-289); the
+ * reference's spurious Delta t^D overflow is not reproduced. */
+sphray_status sphray_accumulate(sphray_context* ctx, int D, size_t nrays, const uint64_t* ray_ids,
+                                const uint64_t* knot_offsets, const int64_t* knot_t,
+                                const int64_t* knot_b, uint64_t* piece_offsets, int64_t* piece_t,
+                                int64_t* piece_a, uint64_t* ops, sphray_error* err);
+
 /* quantize_particle<Int> (quantize.hpp:199-250) for explicit hits: knots of
  * hit i are written at [i*(K+1), i*(K+1)+count_i) with D+1 jumps each. */
 sphray_status sphray_quantize_hits(sphray_context* ctx, const sphray_particle* particles,

@@ -15,6 +15,7 @@
 #include <memory>
 #include <span>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "sphray_gpu.h"
@@ -99,10 +100,19 @@ inline sphray_dataset_stats to_c(const DatasetStats& s) {
             static_cast<uint64_t>(s.count)};
 }
 
-// render_scene<Int>, raycast.hpp:414-497.  Int selects nothing on the device
-// (the path computes exactly in wrapping int64 with Int128-equal results
-// whenever those fit int64); the integer width comes from qc.width like
-// dispatch_int_width (int_ops.hpp:113-121).
+// The device arithmetic for render_scene<Int>: int32_t -> every Checked
+// value must fit int32 (int_width 32); int64_t -> int64 (64); Int128 on
+// quanta of at most 64 bits -> the exact modulo-2^64 merge, which equals the
+// Int128 result whenever that fits int64 and raises OverflowError otherwise
+// (64); Int128 on w128 quanta is not served (ConfigError).
+template <class Int>
+constexpr int device_int_width(int quanta_bits) {
+    if constexpr (std::is_same_v<Int, std::int32_t>) return 32;
+    else if constexpr (std::is_same_v<Int, std::int64_t>) return 64;
+    else return quanta_bits <= 64 ? 64 : 128;
+}
+
+// render_scene<Int>, raycast.hpp:414-497, on the B200 path.
 template <class Int>
 Image render_scene(std::span<const Particle> particles, const Camera& cam,
                    const TransferFunction& tf, const Lut& lut, const QuantaConfig& qc,
@@ -114,7 +124,7 @@ Image render_scene(std::span<const Particle> particles, const Camera& cam,
     std::vector<sphray_tf_point> pts;
     for (const auto& p : tf.points) pts.push_back({p.value, p.r, p.g, p.b, p.absorption});
     const LutRecords L = to_c(lut);
-    const sphray_quanta q{qc.tau, qc.sigma, static_cast<int32_t>(qc.width), 0};
+    const sphray_quanta q{qc.tau, qc.sigma, device_int_width<Int>(static_cast<int>(qc.width)), 0};
     const sphray_dataset_stats ds = to_c(stats);
     sphray_render_options o{};
     o.step = opts.step;

@@ -61,6 +61,27 @@ int main() {
     std::printf("gpu knots %zu rays %zu int_ops %llu residual %zu skipped %zu\n", rs_gpu.knots,
                 rs_gpu.rays_touched, (unsigned long long)rs_gpu.int_ops, rs_gpu.residual_failures,
                 rs_gpu.skipped_particles);
+    // the Int parameter selects the device arithmetic (dispatch_int_width,
+    // int_ops.hpp:113-121): <int32_t> on w32 quanta, <Int128> on w64 quanta
+    const auto qc32 = choose_quanta({4, 3}, kernel_constants(kern), kern.q, stats, IntWidth::w32);
+    RenderStats r32a, r32b, r128a, r128b;
+    const Image c32 = render_scene<std::int32_t>(ps, cam, tf, lut, qc32, stats, opts, &r32a);
+    const Image d32 = gpu::render_scene<std::int32_t>(ps, cam, tf, lut, qc32, stats, opts, &r32b);
+    const Image c128 = render_scene<Int128>(ps, cam, tf, lut, qc, stats, opts, &r128a);
+    const Image d128 = gpu::render_scene<Int128>(ps, cam, tf, lut, qc, stats, opts, &r128b);
+    double err32 = 0.0, err128 = 0.0;
+    for (size_t i = 0; i < c32.pixels.size(); ++i) {
+        err32 = std::max({err32, std::fabs(c32.pixels[i].r - d32.pixels[i].r),
+                          std::fabs(c32.pixels[i].g - d32.pixels[i].g), std::fabs(c32.pixels[i].b - d32.pixels[i].b)});
+        err128 = std::max({err128, std::fabs(c128.pixels[i].r - d128.pixels[i].r),
+                           std::fabs(c128.pixels[i].g - d128.pixels[i].g),
+                           std::fabs(c128.pixels[i].b - d128.pixels[i].b)});
+    }
+    std::printf("int32 max_abs_rgb_diff %.3e knots %zu/%zu; Int128 max_abs_rgb_diff %.3e int_ops %llu/%llu\n",
+                err32, r32a.knots, r32b.knots, err128, (unsigned long long)r128a.int_ops,
+                (unsigned long long)r128b.int_ops);
+    const bool widths_ok = err32 <= 1e-4 && r32a.knots == r32b.knots && r32a.int_ops == r32b.int_ops &&
+                           err128 <= 1e-4 && r128a.int_ops == r128b.int_ops;
     // errors come back as the reference's exception types
     bool threw = false;
     try {
@@ -73,7 +94,7 @@ int main() {
     std::printf("config_error_rethrown %d\n", threw ? 1 : 0);
     const bool ok = err <= 1e-4 && rs_ref.knots == rs_gpu.knots &&
                     rs_ref.rays_touched == rs_gpu.rays_touched &&
-                    rs_ref.int_ops == rs_gpu.int_ops && threw;
+                    rs_ref.int_ops == rs_gpu.int_ops && threw && widths_ok;
     std::printf("%s\n", ok ? "SHIM_OK" : "SHIM_MISMATCH");
     return ok ? 0 : 1;
 }

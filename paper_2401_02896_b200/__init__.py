@@ -224,6 +224,7 @@ def load_library():
                                        P(_Quanta), P(_Error)]
     L.sphray_lut_parse.argtypes = [C.c_void_p, C.c_size_t, P(_LutView), C.c_char_p, P(_Error)]
     L.sphray_generate_scene.argtypes = [C.c_int, C.c_size_t, C.c_uint64, P(_Particle), P(_Error)]
+    L.sphray_accumulate.argtypes = [C.c_void_p, C.c_int, C.c_size_t] + [C.c_void_p] * 8 + [P(_Error)]
     L.sphray_lut_serialize.argtypes = [P(_LutView), C.c_char_p, C.c_void_p, C.c_size_t, P(C.c_size_t),
                                        P(_Error)]
     L.sphray_lut_save.argtypes = [C.c_char_p, P(_LutView), C.c_char_p, P(_Error)]
@@ -238,7 +239,7 @@ def load_library():
                  "sphray_render_scene", "sphray_scene_upload", "sphray_scene_render",
                  "sphray_scene_hits", "sphray_scene_pieces", "sphray_quantize_hits",
                  "sphray_compute_dataset_stats", "sphray_choose_quanta", "sphray_lut_parse",
-                 "sphray_generate_scene", "sphray_lut_serialize", "sphray_lut_save",
+                 "sphray_generate_scene", "sphray_lut_serialize", "sphray_accumulate", "sphray_lut_save",
                  "sphray_render_report"):
         getattr(L, name).restype = C.c_int
     _lib = L
@@ -747,6 +748,29 @@ class Context:
         _check(self._L.sphray_scene_dataset_stats(self._h, clustering_factor, C.byref(out),
                                                   C.byref(err)), err)
         return DatasetStats._from(out)
+
+    def accumulate(self, knot_t, knot_b, D: int, ray_offsets=None, ray_ids=None):
+        """accumulate<int64_t> (raycast.hpp:261-292) for explicit knot streams on
+        the GPU.  knot_t (n,), knot_b (n, <=7) jumps; ray_offsets (nrays+1) CSR
+        (default: one ray), ray_ids for error reports.  Returns
+        (piece_offsets, piece_t, piece_a (P, D+1), ops per ray)."""
+        kt = np.ascontiguousarray(knot_t, np.int64)
+        kb = np.zeros((len(kt), 7), np.int64)
+        b = np.asarray(knot_b, np.int64).reshape(len(kt), -1)
+        kb[:, : b.shape[1]] = b
+        off = np.ascontiguousarray([0, len(kt)] if ray_offsets is None else ray_offsets, np.uint64)
+        nr = len(off) - 1
+        rid = np.ascontiguousarray(np.arange(nr) if ray_ids is None else ray_ids, np.uint64)
+        poff = np.zeros(nr + 1, np.uint64)
+        pt = np.zeros(max(len(kt), 1), np.int64)
+        pa = np.zeros((max(len(kt), 1), D + 1), np.int64)
+        ops = np.zeros(max(nr, 1), np.uint64)
+        err = _Error()
+        P = lambda x: x.ctypes.data_as(C.c_void_p)  # noqa: E731
+        _check(self._L.sphray_accumulate(self._h, int(D), nr, P(rid), P(off), P(kt), P(kb), P(poff), P(pt),
+                                         P(pa), P(ops), C.byref(err)), err)
+        npc = int(poff[-1])
+        return poff, pt[:npc], pa[:npc], ops[:nr]
 
     def quantize_hits(self, particles, t_chi, lam, lut: Lut, qc: QuantaConfig):
         """quantize_particle (quantize.hpp:199-250) for explicit hits (one particle row each)."""

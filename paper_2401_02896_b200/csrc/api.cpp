@@ -383,6 +383,18 @@ sphray_status sphray_scene_dataset_stats(sphray_context* ctx, double clustering_
     });
 }
 
+sphray_status sphray_accumulate(sphray_context* ctx, int D, size_t nrays, const uint64_t* ray_ids,
+                                const uint64_t* knot_offsets, const int64_t* knot_t,
+                                const int64_t* knot_b, uint64_t* piece_offsets, int64_t* piece_t,
+                                int64_t* piece_a, uint64_t* ops, sphray_error* err) {
+    return guarded(err, [&] {
+        Engine& e = engine(ctx);
+        if (nrays && (!ray_ids || !knot_offsets || (knot_offsets[nrays] && (!knot_t || !knot_b))))
+            fail(SPHRAY_ERR_CONFIG, "accumulate: null input");
+        e.accumulate(D, nrays, ray_ids, knot_offsets, knot_t, knot_b, piece_offsets, piece_t, piece_a, ops);
+    });
+}
+
 sphray_status sphray_lut_serialize(const sphray_lut_view* lut, const char* kernel_id, uint8_t* out,
                                    size_t cap, size_t* nbytes, sphray_error* err) {
     return guarded(err, [&] {

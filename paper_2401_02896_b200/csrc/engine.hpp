@@ -73,6 +73,12 @@ class Engine {
                        const double* lam, const sphray_lut_view& lut, const sphray_quanta& qc,
                        int64_t* knot_t, int64_t* knot_b, int32_t* knot_count);
     const double* device_image() const { return d_image_.as<double>(); }
+    // accumulate<int64_t> for explicit knot streams (accumulate.cu)
+    void accumulate(int D, size_t nrays, const uint64_t* ray_ids, const uint64_t* koff, const int64_t* kt,
+                    const int64_t* kb, uint64_t* piece_off, int64_t* piece_t, int64_t* piece_a, uint64_t* ops) {
+        set_device();
+        accumulate_knots(D, nrays, ray_ids, koff, kt, kb, piece_off, piece_t, piece_a, ops, stream_);
+    }
     // pinned host staging for n particle records (file ingestion: the upload
     // from it is a true async DMA); valid until the next call
     sphray_particle* stage_particles(size_t n);

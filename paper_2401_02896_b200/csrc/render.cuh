@@ -204,6 +204,10 @@ void launch_quantize_hits(const QuantParams& Q, int D, const sphray_particle* ps
                           const double* tchi, const double* lam, int64_t* knot_t,
                           int64_t* knot_b, int32_t* knot_count, cudaStream_t s);
 
+// accumulate.cu: accumulate<int64_t> for explicit knot streams (7 jumps per knot)
+void accumulate_knots(int D, size_t nrays, const uint64_t* ray_ids, const uint64_t* koff, const int64_t* kt,
+                      const int64_t* kb, uint64_t* piece_off, int64_t* piece_t, int64_t* piece_a, uint64_t* ops,
+                      cudaStream_t s);
 // sort.cu: hand-written scan and stable LSD radix sort
 size_t scan_tmp_bytes(size_t n);
 void scan_u32(const uint32_t* in, uint32_t* out, size_t n, void* tmp, uint32_t* total_dev, cudaStream_t s);

@@ -144,13 +144,10 @@ __device__ __forceinline__ int sample_count(double len, double step, double inv_
 // glibc's).  Either way alpha is within a few ulps of the reference's, so the
 // early-termination test T <= 1e-3 sees the same transmittance to ~1e-15.
 #ifndef SPHRAY_ALPHA_MODE
-#define SPHRAY_ALPHA_MODE 0  // diagnostics: 1 = round-1 fp32 alpha (4-term series, __expf)
+#define SPHRAY_ALPHA_MODE 2  // 2: series to x^6 below 1/16, fp64 exp above; 0: series to x^8; 1: round-1 fp32 (diagnostics)
 #endif
 #ifndef SPHRAY_OVF_CHECK
-#define SPHRAY_OVF_CHECK 2  // genuine-overflow test of the merge: 2 fp32 high words (fp64 for long steps), 1 fp64, 0 off (diagnostics)
-#endif
-#ifndef SPHRAY_RECORDS
-#define SPHRAY_RECORDS 1  // diagnostics: 0 = no per-ray piece checksum code in the walk
+#define SPHRAY_OVF_CHECK 1  // genuine-overflow test of the merge: 1 fp64, 2 fp32 high words + fp64 for long steps (measured slower), 0 off (diagnostics)
 #endif
 __device__ __forceinline__ double alpha_of(double x) {
     if (SPHRAY_ALPHA_MODE == 1) {
@@ -443,7 +440,10 @@ __device__ __noinline__ ReplayOut replay_run(const FrameParams& P, uint32_t tf_s
 
 // One warp renders one ray at a time.  TS: the transfer function is read
 // from the CTA's shared copy (else from global memory).
-template <int D, int M, bool TS, bool DUMP, bool EVEN>
+// REC: the per-ray records (piece checksums) are compiled in; the production
+// kernel is instantiated with and without them (the checksum code costs ~2% of
+// the frame even when disabled at run time), the robust variant always has them.
+template <int D, int M, bool TS, bool DUMP, bool EVEN, bool REC>
 class RayWorker {
    public:
     static constexpr int KN = 2 * M + 1;  // knots per hit, at most
@@ -544,7 +544,8 @@ class RayWorker {
             if constexpr (DUMP)
 #pragma unroll
                 for (int d = 0; d <= D; ++d) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
-            if (SPHRAY_RECORDS && P.ray_rec && !stop) csum += piece_mix<D>(t, Pc);
+            if constexpr (REC)
+                if (P.ray_rec && !stop) csum += piece_mix<D>(t, Pc);
             if constexpr (DUMP)
                 if (!stop && P.dump_piece_t) dump_piece(t, Pc);
             if (!more) {
@@ -1044,10 +1045,12 @@ class RayWorker {
         const double sr = warp_sum(Cr), sg = warp_sum(Cg), sb = warp_sum(Cb);
         const bool ovf_any = __any_sync(kFull, aovf);
         uint64_t cs = 0;
-        if (P.ray_rec) {
+        if constexpr (REC) {
+            if (P.ray_rec) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(kFull, csum, o);
-            cs = csum;
+                for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(kFull, csum, o);
+                cs = csum;
+            }
         }
         if (lane == 0) {
             double r = P.bg[0], g = P.bg[1], b = P.bg[2];
@@ -1081,7 +1084,7 @@ class RayWorker {
             if (ovf_any) atomicMin(&P.stats[kStatAccumOverflowRay], static_cast<unsigned long long>(ray_id));
             if (hits) atomicAdd(&P.stats[kStatHits], hits);
             atomicMax(&P.stats[kStatMaxPending], static_cast<unsigned long long>(max_pending));
-            if (P.ray_rec) {
+            if (REC && P.ray_rec) {
                 sphray_ray_record rec;
                 rec.piece_checksum = cs;
                 rec.knots = static_cast<uint32_t>(knots);
@@ -1101,7 +1104,7 @@ class RayWorker {
     }
 };
 
-template <int D, int M, bool TS, bool DUMP, bool EVEN>
+template <int D, int M, bool TS, bool DUMP, bool EVEN, bool REC>
 __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const __grid_constant__ FrameParams P) {
     extern __shared__ __align__(16) char smem[];
     const int warp = threadIdx.x >> 5;
@@ -1114,7 +1117,7 @@ __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const __grid_constant_
         __syncthreads();
         tf_sa = static_cast<uint32_t>(__cvta_generic_to_shared(st));
     }
-    RayWorker<D, M, TS, DUMP, EVEN> rw(P, wm, lane, tf_sa);
+    RayWorker<D, M, TS, DUMP, EVEN, REC> rw(P, wm, lane, tf_sa);
     while (true) {
         unsigned long long item = 0;
         if (lane == 0) item = atomicAdd(P.work_counter, 1ull);
@@ -1198,11 +1201,11 @@ __global__ void k_quantize_hits(const QuantParams Q, const sphray_particle* ps, 
 template <int D, int M, bool EVEN>
 int render_occupancy_tt(int warps, size_t smem) {
     int nb = 0;
-    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(rk::k_render_rays<D, M, true, false, EVEN>,
+    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(rk::k_render_rays<D, M, true, false, EVEN, false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
     SPHRAY_RK_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nb, rk::k_render_rays<D, M, true, false, EVEN>, warps * 32, smem));
+        &nb, rk::k_render_rays<D, M, true, false, EVEN, false>, warps * 32, smem));
     return nb;
 }
 
@@ -1219,9 +1222,10 @@ void launch_render_tt(const FrameParams& P, int blocks, int warps, cudaStream_t 
     // the production kernel carries none of it (it is instruction-cache
     // sensitive).  The robust variant reads the transfer function from global.
     const bool robust = P.dump_hit_ray || P.dump_piece_t || P.ray_list || P.robust;
-    auto kern = robust ? rk::k_render_rays<D, M, false, true, EVEN>
-                     : (P.tf_smem ? rk::k_render_rays<D, M, true, false, EVEN>
-                                  : rk::k_render_rays<D, M, false, false, EVEN>);
+    auto kern = robust ? rk::k_render_rays<D, M, false, true, EVEN, true>
+                : P.tf_smem ? (P.ray_rec ? rk::k_render_rays<D, M, true, false, EVEN, true>
+                                         : rk::k_render_rays<D, M, true, false, EVEN, false>)
+                            : rk::k_render_rays<D, M, false, false, EVEN, true>;
     SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
     kern<<<blocks, warps * 32, smem, s>>>(P);

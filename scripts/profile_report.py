@@ -71,6 +71,11 @@ def main():
                                                  "render_kernel.cuh"))
     ap.add_argument("--title", default="render kernel profile")
     ap.add_argument("--out", required=True)
+    ap.add_argument("--evidence", help="also write the bench's profile evidence JSON here")
+    ap.add_argument("--knots", type=float, default=0.0, help="knots of the captured launch")
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--res", type=int, default=2048)
+    ap.add_argument("--source", default="")
     a = ap.parse_args()
     md = [f"# {a.title}", ""]
     if a.rep:
@@ -91,6 +96,7 @@ def main():
             ("DRAM write bytes", "dram__bytes_write.sum", 1),
             ("L2 hit %", "lts__t_sector_hit_rate.pct", 1),
             ("registers / thread", "launch__registers_per_thread", 1),
+            ("thread instructions executed", "smsp__thread_inst_executed.sum", 1),
         ]
         md += ["## Key metrics", "", "| metric | value |", "|---|---|"]
         for name, k, sc in keys:
@@ -103,6 +109,28 @@ def main():
         md += ["", "## Stall reasons (PC sampling)", "", "| reason | share |", "|---|---|"]
         for v, k in sorted(st, reverse=True)[:10]:
             md.append(f"| {k} | {v / tot * 100:.1f}% |")
+        wi, ti = fnum(d, "smsp__inst_executed.sum"), fnum(d, "smsp__thread_inst_executed.sum")
+        if wi and ti:
+            md += ["", f"Average active threads per executed warp instruction: {ti / wi:.1f} of 32."]
+        if a.knots and wi:
+            md += [f"Warp instructions per knot: {wi / a.knots:.1f} ({a.knots:.4g} knots in the launch)."]
+        if a.evidence:
+            import json
+            ev = {"config": a.config, "res": a.res, "world": 1, "source": a.source or a.rep,
+                  "dram_bytes": (fnum(d, "dram__bytes_read.sum") or 0) + (fnum(d, "dram__bytes_write.sum") or 0),
+                  "duration_ms": fnum(d, "gpu__time_duration.sum"),
+                  "issue_slots_busy_pct": fnum(d, "sm__instruction_throughput.avg.pct_of_peak_sustained_active"),
+                  "ipc": fnum(d, "sm__inst_executed.avg.per_cycle_active"),
+                  "warps_active_per_sm": fnum(d, "sm__warps_active.avg.per_cycle_active"),
+                  "achieved_occupancy_pct": fnum(d, "sm__warps_active.avg.pct_of_peak_sustained_active"),
+                  "fp64_pipe_pct": fnum(d, "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                  "alu_pipe_pct": fnum(d, "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                  "fma_pipe_pct": fnum(d, "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+                  "lsu_pipe_pct": fnum(d, "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+                  "active_threads_per_warp_inst": (ti / wi) if wi and ti else None,
+                  "warp_instructions_per_knot": (wi / a.knots) if a.knots and wi else None,
+                  "stalls_pct": {k: round(v / tot * 100, 2) for v, k in sorted(st, reverse=True)[:8]}}
+            json.dump(ev, open(a.evidence, "w"), indent=1)
         if a.cubin:
             sass = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv",
                                    "--print-source", "sass"], capture_output=True, text=True).stdout
