@@ -753,7 +753,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
             d_vals2_.ensure(entries * 4);
             d_tmp_.ensure(radix_tmp_bytes(entries));
             launch_emit(pp, order, d_offsets_.as<uint32_t>(), d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(), s);
-            const int end_bit = bits_for(owned_max);
+            const int end_bit = bits_for(owned_max - 1);  // tile keys are < owned_max
             const bool k2 = sort_pairs_u32(d_keys_.as<uint32_t>(), d_keys2_.as<uint32_t>(), d_vals_.as<uint32_t>(),
                                            d_vals2_.as<uint32_t>(), entries, end_bit, d_tmp_.p, s);
             const uint32_t* cand = k2 ? d_vals2_.as<uint32_t>() : d_vals_.as<uint32_t>();

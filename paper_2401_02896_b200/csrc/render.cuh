@@ -17,6 +17,13 @@ constexpr int kHitQueue = 64;
 constexpr int kTfPoint = 10;  // doubles per transfer-function point on the device
 constexpr int kMaxJ = kMaxM * kMaxDegree;
 
+// SPHRAY_STAGE=1: each warp prefetches its next 32 candidate records into
+// shared memory with cp.async.bulk (TMA bulk copy) completing on an mbarrier,
+// one gather step ahead of the hit tests.
+#ifndef SPHRAY_STAGE
+#define SPHRAY_STAGE 0
+#endif
+
 #ifdef __CUDACC__
 #define SPHRAY_HD __host__ __device__
 #else
@@ -35,6 +42,9 @@ SPHRAY_HD inline size_t warp_bytes_for(int D, int cap) {
     b += align16(sizeof(int32_t) * kHitQueue);        // hit queue: particle
     b += align16(sizeof(uint16_t) * cap * 2);         // ps, fl (+ flush set)
     b += align16(sizeof(uint32_t) * 256);             // radix bins
+#if SPHRAY_STAGE
+    b += 32 * 16 + 32 * 32 + 16;                      // staged candidate records + mbarrier
+#endif
     return b;
 }
 

@@ -146,6 +146,9 @@ __device__ __forceinline__ int sample_count(double len, double step, double inv_
 #ifndef SPHRAY_ALPHA_MODE
 #define SPHRAY_ALPHA_MODE 2  // 2: series to x^6 below 1/16, fp64 exp above; 0: series to x^8; 1: round-1 fp32 (diagnostics)
 #endif
+#ifndef SPHRAY_OVF_CARRY
+#define SPHRAY_OVF_CARRY 1  // the walk keeps the last piece as doubles (shared by the overflow test and compositing)
+#endif
 #ifndef SPHRAY_OVF_CHECK
 #define SPHRAY_OVF_CHECK 1  // genuine-overflow test of the merge: 1 fp64, 2 fp32 high words + fp64 for long steps (measured slower), 0 off (diagnostics)
 #endif
@@ -272,6 +275,9 @@ struct WarpMem {
     uint16_t* ps;   // pending slots, unsorted
     uint16_t* fl;   // free slot stack (+ the flush set above it)
     uint32_t* hist;  // 256: radix-sort bins
+    uint4* st_meta;   // SPHRAY_STAGE: 32 staged candidate records {front, particle, bbox, 0}
+    double4* st_xyzh; //               and their {x, y, z, h}
+    uint64_t* bar;    //               the mbarrier their bulk copy completes on
 };
 
 __device__ inline WarpMem carve(char* base, int D, int cap) {
@@ -293,7 +299,37 @@ __device__ inline WarpMem carve(char* base, int D, int cap) {
     w.fl = w.ps + cap;
     p += align16(sizeof(uint16_t) * cap * 2);
     w.hist = reinterpret_cast<uint32_t*>(p);
+    p += align16(sizeof(uint32_t) * 256);
+    w.st_meta = reinterpret_cast<uint4*>(p);
+    p += 32 * 16;
+    w.st_xyzh = reinterpret_cast<double4*>(p);
+    p += 32 * 32;
+    w.bar = reinterpret_cast<uint64_t*>(p);
     return w;
+}
+
+// cp.async.bulk (bulk TMA) of candidate records into shared memory, completing
+// on an mbarrier (transaction count = bytes).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(phase)
+        : "memory");
 }
 
 // Piece compositing (composite(), raycast.hpp:356-381), shared by the lane
@@ -353,6 +389,16 @@ struct Compositor {
     __device__ __forceinline__ int piece_setup(int64_t ts, int64_t te, const uint64_t (&a)[D + 1],
                                                double (&c)[D + 1], double& x0, double& dx,
                                                double& dt) const {
+        double A[D + 1];
+#pragma unroll
+        for (int d = 0; d <= D; ++d) A[d] = static_cast<double>(static_cast<int64_t>(a[d]));
+        return piece_setup_d(ts, te, A, c, x0, dx, dt);
+    }
+    // the same from the coefficients already converted to double (exact
+    // integers up to rounding; zero exactly when the integer is zero)
+    __device__ __forceinline__ int piece_setup_d(int64_t ts, int64_t te, const double (&A)[D + 1],
+                                                 double (&c)[D + 1], double& x0, double& dx,
+                                                 double& dt) const {
         const double a_lo = dmul(static_cast<double>(ts), P.Q.tau);
         const double a_hi = dmul(static_cast<double>(te), P.Q.tau);
         const double lo = (a_lo < P.cam.near_plane) ? P.cam.near_plane : a_lo;
@@ -364,8 +410,8 @@ struct Compositor {
         bool zero = true;
 #pragma unroll
         for (int d = 0; d <= D; ++d) {
-            zero &= a[d] == 0;
-            c[d] = static_cast<double>(static_cast<int64_t>(a[d])) * P.Q.sigma;
+            zero &= A[d] == 0.0;
+            c[d] = A[d] * P.Q.sigma;
         }
         if (zero && P.tf0_clear) return 0;
         x0 = fma(lo, P.inv_tau, -static_cast<double>(ts));
@@ -377,8 +423,16 @@ struct Compositor {
     __device__ __forceinline__ void composite_piece(int64_t ts, int64_t te, const uint64_t (&a)[D + 1],
                                                     bool stop, double& Tl, double& cr, double& cg,
                                                     double& cb, int& nsmp) const {
+        double A[D + 1];
+#pragma unroll
+        for (int d = 0; d <= D; ++d) A[d] = static_cast<double>(static_cast<int64_t>(a[d]));
+        composite_piece_d(ts, te, A, stop, Tl, cr, cg, cb, nsmp);
+    }
+    __device__ __forceinline__ void composite_piece_d(int64_t ts, int64_t te, const double (&A)[D + 1],
+                                                      bool stop, double& Tl, double& cr, double& cg,
+                                                      double& cb, int& nsmp) const {
         double c[D + 1], x0 = 0.0, dx = 0.0, dt = 0.0;
-        const int n = piece_setup(ts, te, a, c, x0, dx, dt);
+        const int n = piece_setup_d(ts, te, A, c, x0, dx, dt);
         if (n == 0) return;
         nsmp += n;
         double To, r, g, b;
@@ -469,6 +523,8 @@ class RayWorker {
     int max_resid = 0;  // SPHRAY_KSTATS: largest pending set left by a flush
     uint64_t csum = 0;  // per-lane share of the ray's piece checksum (P.ray_rec)
     bool aovf = false;  // a merged coefficient left int64 (shift_overflows / add_checked)
+    uint32_t st_phase = 0;  // SPHRAY_STAGE: parity of the staging mbarrier
+    bool st_inflight = false;
 
     Compositor<D, TS> cmp;
 
@@ -520,16 +576,27 @@ class RayWorker {
         if (lead && comp) cmp.composite_piece(ot, tcur, oa, stop, Tl, cr, cg, cb, nsmp);
         taylor_shift<D>(Pc, static_cast<uint64_t>(tcur) - static_cast<uint64_t>(tref));
         int64_t tn = tcur;
+        // the last emitted piece's coefficients as doubles: the overflow test's
+        // input for the next shift and the compositing input (one conversion)
+        double A[D + 1];
+#pragma unroll
+        for (int d = 0; d <= D; ++d) A[d] = 0.0;
         for (int k = k0; k < k1; ++k) {
             const int s = fs[k];
             const int64_t t = tn;
             if (t != tcur) {
                 const uint64_t dl = static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur);
-                uint64_t before[D + 1];
+                if (SPHRAY_OVF_CARRY) {
+                    taylor_shift<D>(Pc, dl);  // every shift follows an emission in this run
+                    if (SPHRAY_OVF_CHECK)
+                        aovf |= shift_overflows<D>(A, static_cast<double>(static_cast<int64_t>(dl)), Pc);
+                } else {
+                    uint64_t before[D + 1];
 #pragma unroll
-                for (int d = 0; d <= D; ++d) before[d] = Pc[d];
-                taylor_shift<D>(Pc, dl);
-                aovf |= step_overflows<D>(before, dl, Pc);
+                    for (int d = 0; d <= D; ++d) before[d] = Pc[d];
+                    taylor_shift<D>(Pc, dl);
+                    aovf |= step_overflows<D>(before, dl, Pc);
+                }
                 tcur = t;
             }
 #pragma unroll
@@ -541,6 +608,9 @@ class RayWorker {
             tn = more ? pool_t(fs[k + 1]) : t;
             if (more && tn == t) continue;  // more jumps at this position
             ++npc;
+            if (SPHRAY_OVF_CARRY)
+#pragma unroll
+                for (int d = 0; d <= D; ++d) A[d] = static_cast<double>(static_cast<int64_t>(Pc[d]));
             if constexpr (DUMP)
 #pragma unroll
                 for (int d = 0; d <= D; ++d) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
@@ -555,7 +625,10 @@ class RayWorker {
                     for (int d = 0; d <= D; ++d) w.open[1 + d] = Pc[d];
                 }
             } else if (comp) {
-                cmp.composite_piece(t, tn, Pc, stop, Tl, cr, cg, cb, nsmp);
+                if (SPHRAY_OVF_CARRY)
+                    cmp.composite_piece_d(t, tn, A, stop, Tl, cr, cg, cb, nsmp);
+                else
+                    cmp.composite_piece(t, tn, Pc, stop, Tl, cr, cg, cb, nsmp);
             }
         }
     }
@@ -936,8 +1009,31 @@ class RayWorker {
         hq_n = rest;
     }
 
+    // Prefetch the candidate records [c0, min(c0 + 32, ce)) into the warp's
+    // staging buffer (one elected lane issues the two bulk copies).
+    __device__ __forceinline__ void stage_issue(uint32_t c0, uint32_t ce) {
+        if (lane == 0) {
+            const uint32_t nrec = min(32u, ce - c0);
+            const uint32_t bar = smem_addr(w.bar);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bar, nrec * 48u);
+            bulk_g2s(smem_addr(w.st_meta), P.cmeta + c0, nrec * 16u, bar);
+            bulk_g2s(smem_addr(w.st_xyzh), P.cxyzh + c0, nrec * 32u, bar);
+        }
+        st_inflight = true;
+    }
+    __device__ __forceinline__ void stage_wait() {
+        mbar_wait(smem_addr(w.bar), st_phase);
+        st_phase ^= 1u;
+        st_inflight = false;
+    }
+    __device__ __forceinline__ void stage_drain() {
+        if (SPHRAY_STAGE && st_inflight) stage_wait();
+    }
+
     // One ray; returns false if the knot window overflowed (ray is retried).
     __device__ bool run(int px, int py) {
+        stage_drain();
         reset();
         const RayD ray = make_ray(P.cam, px, py);
         const int tile = (py >> kTileShift) * P.tiles_x + (px >> kTileShift);
@@ -947,6 +1043,7 @@ class RayWorker {
         const double near_plane = P.cam.near_plane, far_plane = P.cam.far_plane;
         uint32_t cursor = cb;
         int hq_n = 0;
+        if (SPHRAY_STAGE && cursor < ce) stage_issue(cursor, ce);
         while (true) {
             // ---- gather: exact hit test of 32 candidates at a time
             while (hq_n < SPHRAY_GATHER_TO && hq_n <= kHitQueue - 32 && cursor < ce) {
@@ -955,11 +1052,25 @@ class RayWorker {
                 bool hit = false;
                 double d2 = 0.0, tchi = 0.0;
                 uint32_t pi = 0;
-                if (c < ce) {
+                uint4 mt = make_uint4(0u, 0u, 0u, 0u);
+                double4 p = make_double4(0.0, 0.0, 0.0, 0.0);
+                if (SPHRAY_STAGE) {
+                    // records staged by the previous step's bulk copy; the next
+                    // batch is requested as soon as this one is in registers
+                    stage_wait();
+                    if (c < ce) {
+                        mt = w.st_meta[lane];
+                        p = w.st_xyzh[lane];
+                    }
+                    __syncwarp();
+                    if (cursor + 32 < ce) stage_issue(cursor + 32, ce);
+                } else if (c < ce) {
                     // the tile's candidate record (coalesced: consecutive lanes read
                     // consecutive records, both loads issued together)
-                    const uint4 mt = P.cmeta[c];
-                    const double4 p = P.cxyzh[c];
+                    mt = P.cmeta[c];
+                    p = P.cxyzh[c];
+                }
+                if (c < ce) {
                     pi = mt.y;
                     if (lx >= (mt.z & 15u) && lx <= ((mt.z >> 4) & 15u) && ly >= ((mt.z >> 8) & 15u) &&
                         ly <= ((mt.z >> 12) & 15u))
@@ -1118,6 +1229,8 @@ __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const __grid_constant_
         tf_sa = static_cast<uint32_t>(__cvta_generic_to_shared(st));
     }
     RayWorker<D, M, TS, DUMP, EVEN, REC> rw(P, wm, lane, tf_sa);
+    if (SPHRAY_STAGE && lane == 0) mbar_init(smem_addr(wm.bar));
+    __syncwarp();
     while (true) {
         unsigned long long item = 0;
         if (lane == 0) item = atomicAdd(P.work_counter, 1ull);
@@ -1154,6 +1267,7 @@ __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const __grid_constant_
         }
         __syncwarp();
     }
+    rw.stage_drain();  // no bulk copy may still target this CTA's shared memory
 }
 
 // quantize_particle for explicit hits (validation entry point).

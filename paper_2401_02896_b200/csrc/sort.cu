@@ -31,8 +31,6 @@ constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;  // 8192
 constexpr int kSortWarps = 8;
 constexpr int kSortThreads = kSortWarps * 32;
-constexpr int kSortRounds = 16;                          // 32-item rounds per warp
-constexpr int kSortTile = kSortThreads * kSortRounds;    // 4096 items per CTA
 
 #define SORT_CUDA_OK(x)                                                            \
     do {                                                                           \
@@ -128,15 +126,26 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(const T* in, T* out,
 }
 
 // ---------------------------------------------------------------- radix sort
+// Items per CTA tile: 4096 for 32-bit keys, 2048 for 64-bit keys (the tile is
+// reordered in shared memory before it is written out).
+template <class K>
+constexpr int sort_rounds() {
+    return sizeof(K) == 8 ? 8 : 16;
+}
+template <class K>
+constexpr int sort_tile() {
+    return kSortThreads * sort_rounds<K>();
+}
+
 template <class K>
 __global__ void __launch_bounds__(kSortThreads) k_digit_hist(const K* keys, size_t n, int shift,
                                                              uint32_t* counts, uint32_t tiles) {
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
     __syncthreads();
-    const size_t base = static_cast<size_t>(blockIdx.x) * kSortTile;
+    const size_t base = static_cast<size_t>(blockIdx.x) * sort_tile<K>();
 #pragma unroll 4
-    for (int k = 0; k < kSortRounds; ++k) {
+    for (int k = 0; k < sort_rounds<K>(); ++k) {
         const size_t i = base + static_cast<size_t>(k) * kSortThreads + threadIdx.x;
         if (i < n) atomicAdd(&h[static_cast<uint32_t>(keys[i] >> shift) & 255u], 1u);
     }
@@ -144,20 +153,28 @@ __global__ void __launch_bounds__(kSortThreads) k_digit_hist(const K* keys, size
     counts[static_cast<size_t>(threadIdx.x) * tiles + blockIdx.x] = h[threadIdx.x];
 }
 
+// Stable scatter of one tile: each warp ranks its consecutive items per digit
+// (__match_any_sync rounds of 32, in order); the tile is reordered by digit in
+// shared memory and written out as contiguous runs (coalesced stores).
 template <class K, bool VALS>
 __global__ void __launch_bounds__(kSortThreads) k_digit_scatter(const K* kin, K* kout, const uint32_t* vin,
                                                                 uint32_t* vout, size_t n, int shift,
                                                                 const uint32_t* offsets, uint32_t tiles) {
-    __shared__ uint32_t wc[kSortWarps][256];  // per-warp digit counters, then offsets
+    constexpr int R = sort_rounds<K>(), T = sort_tile<K>();
+    __shared__ uint32_t wc[kSortWarps][256];  // per-warp digit counters, then offsets within the digit
+    __shared__ uint32_t dstart[256], gbase[256], wsum[33];
+    __shared__ K skey[T];
+    __shared__ uint32_t sval[VALS ? T : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kSortWarps * 256; i += kSortThreads) (&wc[0][0])[i] = 0;
     __syncthreads();
-    const size_t base = static_cast<size_t>(blockIdx.x) * kSortTile + static_cast<size_t>(warp) * (32 * kSortRounds);
-    K key[kSortRounds];
-    uint32_t val[kSortRounds];
-    uint32_t rank[kSortRounds];
+    const size_t tile0 = static_cast<size_t>(blockIdx.x) * T;
+    const size_t base = tile0 + static_cast<size_t>(warp) * (32 * R);
+    K key[R];
+    uint32_t val[R];
+    uint32_t rank[R];
 #pragma unroll
-    for (int r = 0; r < kSortRounds; ++r) {
+    for (int r = 0; r < R; ++r) {
         const size_t i = base + static_cast<size_t>(r) * 32 + lane;
         const bool ok = i < n;
         key[r] = ok ? kin[i] : K(0);
@@ -171,26 +188,40 @@ __global__ void __launch_bounds__(kSortThreads) k_digit_scatter(const K* kin, K*
         __syncwarp();
     }
     __syncthreads();
-    {  // per digit: exclusive prefix over the warps, plus the global base of (digit, tile)
+    uint32_t cnt;
+    {  // per digit: exclusive prefix over the warps; the tile's count and global base
         const int d = threadIdx.x;
-        uint32_t run = offsets[static_cast<size_t>(d) * tiles + blockIdx.x];
+        uint32_t run = 0;
 #pragma unroll
         for (int w = 0; w < kSortWarps; ++w) {
             const uint32_t c = wc[w][d];
             wc[w][d] = run;
             run += c;
         }
+        cnt = run;
+        gbase[d] = offsets[static_cast<size_t>(d) * tiles + blockIdx.x];
     }
+    uint32_t total;
+    dstart[threadIdx.x] = block_excl(cnt, wsum, total);  // syncs inside
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kSortRounds; ++r) {
+    for (int r = 0; r < R; ++r) {
         const size_t i = base + static_cast<size_t>(r) * 32 + lane;
         if (i < n) {
             const uint32_t dg = static_cast<uint32_t>(key[r] >> shift) & 255u;
-            const uint32_t at = wc[warp][dg] + rank[r];
-            kout[at] = key[r];
-            if constexpr (VALS) vout[at] = val[r];
+            const uint32_t at = dstart[dg] + wc[warp][dg] + rank[r];
+            skey[at] = key[r];
+            if constexpr (VALS) sval[at] = val[r];
         }
+    }
+    __syncthreads();
+    const uint32_t valid = static_cast<uint32_t>(n - tile0 < static_cast<size_t>(T) ? n - tile0 : T);
+    for (uint32_t i = threadIdx.x; i < valid; i += kSortThreads) {
+        const K k = skey[i];
+        const uint32_t dg = static_cast<uint32_t>(k >> shift) & 255u;
+        const uint32_t at = gbase[dg] + (i - dstart[dg]);
+        kout[at] = k;
+        if constexpr (VALS) vout[at] = sval[i];
     }
 }
 
@@ -218,7 +249,7 @@ void sort_impl(K* k0, K* k1, uint32_t* v0, uint32_t* v1, size_t n, int end_bit, 
     result_in_first = true;
     if (n == 0) return;
     if (n >= 0xffffffffull) fail(SPHRAY_ERR_CAPACITY, "radix sort: more than 2^32 - 1 items");
-    const uint32_t tiles = grid_of(n, kSortTile);
+    const uint32_t tiles = grid_of(n, sort_tile<K>());
     const size_t m = static_cast<size_t>(256) * tiles;
     uint32_t* counts = static_cast<uint32_t*>(tmp);
     uint32_t* stmp = counts + m;
@@ -250,7 +281,8 @@ void scan_u32(const uint32_t* in, uint32_t* out, size_t n, void* tmp, uint32_t* 
 }
 
 size_t radix_tmp_bytes(size_t n) {
-    const size_t tiles = grid_of(n, kSortTile);
+    const size_t tiles = grid_of(n, sort_tile<uint32_t>() < sort_tile<unsigned long long>()
+                                        ? sort_tile<uint32_t>() : sort_tile<unsigned long long>());
     const size_t m = 256 * tiles;
     return (m + scan_tmp_elems<uint32_t>(m)) * sizeof(uint32_t) + 16;
 }
