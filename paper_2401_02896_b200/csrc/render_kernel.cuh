@@ -94,7 +94,9 @@ __device__ __forceinline__ int64_t knot_floor(float front, double inv_tau) {
 // which reproduces the end point exactly.
 constexpr int kTfStride = kTfPoint;
 
-// TF readers: the per-CTA shared copy (ld.shared) or global memory.
+// TF readers: the per-CTA shared copy (ld.shared) or global memory; a point's
+// 10 doubles are 16-byte aligned, read in pairs (value, r) (g, b) (ab, sr)
+// (sg, sb) (sab, pad).
 struct TfShared {
     uint32_t base;
     __device__ __forceinline__ double operator()(int k) const {
@@ -102,10 +104,18 @@ struct TfShared {
         asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(base + 8u * static_cast<uint32_t>(k)));
         return v;
     }
+    __device__ __forceinline__ double2 pair(int k) const {
+        double2 v;
+        asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(base + 8u * static_cast<uint32_t>(k)));
+        return v;
+    }
 };
 struct TfGlobal {
     const double* p;
     __device__ __forceinline__ double operator()(int k) const { return __ldg(p + k); }
+    __device__ __forceinline__ double2 pair(int k) const {
+        return __ldg(reinterpret_cast<const double2*>(p + k));
+    }
 };
 
 template <class Ld>
@@ -120,11 +130,13 @@ __device__ __forceinline__ void tf_sample(const Ld& ld, int n, double v, double&
         a = i - kTfStride;
     }
     if (hi) a = last;
-    const double w = (lo || hi) ? 0.0 : v - ld(a);
-    r = fma(w, ld(a + 5), ld(a + 1));
-    g = fma(w, ld(a + 6), ld(a + 2));
-    b = fma(w, ld(a + 7), ld(a + 3));
-    ab = fma(w, ld(a + 8), ld(a + 4));
+    const double2 p0 = ld.pair(a), p1 = ld.pair(a + 2), p2 = ld.pair(a + 4), p3 = ld.pair(a + 6),
+                  p4 = ld.pair(a + 8);
+    const double w = (lo || hi) ? 0.0 : v - p0.x;
+    r = fma(w, p2.y, p0.y);
+    g = fma(w, p3.x, p1.x);
+    b = fma(w, p3.y, p1.y);
+    ab = fma(w, p4.x, p2.x);
 }
 
 // n = max(2, ceil((hi - lo) / step)) exactly as the reference counts samples
@@ -152,12 +164,30 @@ __device__ __forceinline__ int sample_count(double len, double step, double inv_
 #ifndef SPHRAY_OVF_CHECK
 #define SPHRAY_OVF_CHECK 1  // genuine-overflow test of the merge: 1 fp64, 2 fp32 high words + fp64 for long steps (measured slower), 0 off (diagnostics)
 #endif
+#ifndef SPHRAY_COLD_OUTLINE
+#define SPHRAY_COLD_OUTLINE 0  // rarely executed code out of line (the kernel is instruction-cache bound)
+#endif
+// 1 - exp(-x) for x >= 1/16: CUDA's fp64 exp is several hundred SASS
+// instructions; out of line it stays out of the hot loop's instruction cache.
+static __device__ __noinline__ double one_minus_exp_neg_ool(double x) { return 1.0 - exp(-x); }
+__device__ __forceinline__ double one_minus_exp_neg(double x) {
+    if (SPHRAY_COLD_OUTLINE) return one_minus_exp_neg_ool(x);
+    return 1.0 - exp(-x);
+}
 __device__ __forceinline__ double alpha_of(double x) {
     if (SPHRAY_ALPHA_MODE == 1) {
         if (x < 0.05) return x * (1.0 - x * (0.5 - x * (1.0 / 6.0 - x * (1.0 / 24.0))));
         return 1.0 - static_cast<double>(__expf(-static_cast<float>(x)));
     }
-    if (SPHRAY_ALPHA_MODE == 2) {  // series to x^6 below 1/16 (relative error < 7e-13)
+    if (SPHRAY_ALPHA_MODE == 2) {  // series to x^4 below 2^-8, to x^6 below 1/16 (relative error < 7e-13)
+        if (x < 0x1p-8) {
+            double s = 1.0 / 120.0;
+            s = fma(s, -x, 1.0 / 24.0);
+            s = fma(s, -x, 1.0 / 6.0);
+            s = fma(s, -x, 0.5);
+            s = fma(s, -x, 1.0);
+            return s * x;
+        }
         if (x < 0.0625) {
             double s = 1.0 / 5040.0;
             s = fma(s, -x, 1.0 / 720.0);
@@ -168,7 +198,7 @@ __device__ __forceinline__ double alpha_of(double x) {
             s = fma(s, -x, 1.0);
             return s * x;
         }
-        return 1.0 - exp(-x);
+        return one_minus_exp_neg(x);
     }
     if (x < 0.0625) {
         double s = 1.0 / 40320.0;
@@ -181,7 +211,7 @@ __device__ __forceinline__ double alpha_of(double x) {
         s = fma(s, -x, 1.0);
         return s * x;
     }
-    return 1.0 - exp(-x);
+    return one_minus_exp_neg(x);
 }
 
 // sphray_piece_mix (include/sphray_gpu.h) of one FieldPiece, for the per-ray
