@@ -76,7 +76,13 @@ typedef struct sphray_lut_view {
     const double* records;
 } sphray_lut_view;
 
-/* sphray::QuantaConfig (quantize.hpp:44-51). int_width: 32, 64 or 128. */
+/* sphray::QuantaConfig (quantize.hpp:44-51). int_width: 32, 64 or 128 -- the
+ * device arithmetic, as render_scene<Int> with Int of that width:
+ * 32: every Checked value and merged coefficient must fit int32;
+ * 64: int64 (the production kernel);
+ * 128: 128-bit jumps and a modulo-2^128 merge (knot positions must fit int64,
+ *      else SPHRAY_ERR_CAPACITY; validation outputs are int64 only).
+ * A genuine overflow of the width raises SPHRAY_ERR_OVERFLOW naming the ray. */
 typedef struct sphray_quanta {
     double tau;
     double sigma;

@@ -104,7 +104,8 @@ inline sphray_dataset_stats to_c(const DatasetStats& s) {
 // value must fit int32 (int_width 32); int64_t -> int64 (64); Int128 on
 // quanta of at most 64 bits -> the exact modulo-2^64 merge, which equals the
 // Int128 result whenever that fits int64 and raises OverflowError otherwise
-// (64); Int128 on w128 quanta is not served (ConfigError).
+// (64); Int128 on w128 quanta -> 128-bit jumps and a modulo-2^128 merge (128;
+// knot positions must fit int64, else CapacityError).
 template <class Int>
 constexpr int device_int_width(int quanta_bits) {
     if constexpr (std::is_same_v<Int, std::int32_t>) return 32;

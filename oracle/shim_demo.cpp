@@ -80,8 +80,20 @@ int main() {
     std::printf("int32 max_abs_rgb_diff %.3e knots %zu/%zu; Int128 max_abs_rgb_diff %.3e int_ops %llu/%llu\n",
                 err32, r32a.knots, r32b.knots, err128, (unsigned long long)r128a.int_ops,
                 (unsigned long long)r128b.int_ops);
+    // <Int128> on w128 quanta: the device's 128-bit merge
+    const auto qcw = choose_quanta({4, 3}, kernel_constants(kern), kern.q, stats, IntWidth::w128);
+    RenderStats rwa, rwb;
+    const Image cw = render_scene<Int128>(ps, cam, tf, lut, qcw, stats, opts, &rwa);
+    const Image dw = gpu::render_scene<Int128>(ps, cam, tf, lut, qcw, stats, opts, &rwb);
+    double errw = 0.0;
+    for (size_t i = 0; i < cw.pixels.size(); ++i)
+        errw = std::max({errw, std::fabs(cw.pixels[i].r - dw.pixels[i].r), std::fabs(cw.pixels[i].g - dw.pixels[i].g),
+                         std::fabs(cw.pixels[i].b - dw.pixels[i].b)});
+    std::printf("Int128/w128 max_abs_rgb_diff %.3e knots %zu/%zu int_ops %llu/%llu\n", errw, rwa.knots, rwb.knots,
+                (unsigned long long)rwa.int_ops, (unsigned long long)rwb.int_ops);
     const bool widths_ok = err32 <= 1e-4 && r32a.knots == r32b.knots && r32a.int_ops == r32b.int_ops &&
-                           err128 <= 1e-4 && r128a.int_ops == r128b.int_ops;
+                           err128 <= 1e-4 && r128a.int_ops == r128b.int_ops && errw <= 1e-4 &&
+                           rwa.knots == rwb.knots && rwa.int_ops == rwb.int_ops;
     // errors come back as the reference's exception types
     bool threw = false;
     try {

@@ -756,8 +756,9 @@ class Context:
         (piece_offsets, piece_t, piece_a (P, D+1), ops per ray)."""
         kt = np.ascontiguousarray(knot_t, np.int64)
         kb = np.zeros((len(kt), 7), np.int64)
-        b = np.asarray(knot_b, np.int64).reshape(len(kt), -1)
-        kb[:, : b.shape[1]] = b
+        if len(kt):
+            b = np.asarray(knot_b, np.int64).reshape(len(kt), -1)
+            kb[:, : b.shape[1]] = b
         off = np.ascontiguousarray([0, len(kt)] if ray_offsets is None else ray_offsets, np.uint64)
         nr = len(off) - 1
         rid = np.ascontiguousarray(np.arange(nr) if ray_ids is None else ray_ids, np.uint64)

@@ -280,5 +280,81 @@ __device__ __forceinline__ void taylor_shift(uint64_t (&v)[D + 1], uint64_t delt
         for (int j = D - 1; j >= i; --j) v[j] += delta * v[j + 1];
 }
 
+// The same modulo 2^128 (render_scene<Int128>, int_width 128); delta is a
+// wrapped int64 position difference, sign-extended.
+template <int D>
+__device__ __forceinline__ void taylor_shift(unsigned __int128 (&v)[D + 1], uint64_t delta) {
+    const unsigned __int128 dl =
+        static_cast<unsigned __int128>(static_cast<__int128>(static_cast<int64_t>(delta)));
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = D - 1; j >= i; --j) v[j] += dl * v[j + 1];
+}
+
+// ---------------------------------------------------------------------------
+// Checked<Int128> (int_ops.hpp:63-99): wrapping __int128 arithmetic plus an
+// overflow flag, for int_width 128 (quantize.hpp:199-250 with Int = Int128).
+using i128 = __int128;
+using u128 = unsigned __int128;
+constexpr i128 kI128Min = static_cast<i128>(static_cast<u128>(1) << 127);
+
+__device__ __forceinline__ i128 cadd(i128 a, i128 b, bool& o) {
+    const i128 r = static_cast<i128>(static_cast<u128>(a) + static_cast<u128>(b));
+    o |= ((a ^ r) & (b ^ r)) < 0;
+    return r;
+}
+__device__ __forceinline__ i128 csub(i128 a, i128 b, bool& o) {
+    const i128 r = static_cast<i128>(static_cast<u128>(a) - static_cast<u128>(b));
+    o |= ((a ^ b) & (a ^ r)) < 0;
+    return r;
+}
+__device__ __forceinline__ i128 cneg(i128 a, bool& o) {
+    o |= a == kI128Min;
+    return static_cast<i128>(static_cast<u128>(0) - static_cast<u128>(a));
+}
+// a * b, exact or flagged: magnitudes split in 64-bit limbs
+__device__ __forceinline__ i128 cmul(i128 a, i128 b, bool& o) {
+    const bool neg = (a < 0) != (b < 0);
+    const u128 ua = a < 0 ? static_cast<u128>(0) - static_cast<u128>(a) : static_cast<u128>(a);
+    const u128 ub = b < 0 ? static_cast<u128>(0) - static_cast<u128>(b) : static_cast<u128>(b);
+    const uint64_t ah = static_cast<uint64_t>(ua >> 64), al = static_cast<uint64_t>(ua);
+    const uint64_t bh = static_cast<uint64_t>(ub >> 64), bl = static_cast<uint64_t>(ub);
+    bool big = ah != 0 && bh != 0;
+    const u128 cross = static_cast<u128>(ah) * bl + static_cast<u128>(al) * bh;  // < 2^128 when !big
+    big |= (cross >> 64) != 0;
+    const u128 lo = static_cast<u128>(al) * bl;
+    const u128 mag = lo + (cross << 64);
+    big |= mag < lo;
+    big |= neg ? mag > (static_cast<u128>(1) << 127) : (mag >> 127) != 0;
+    o |= big;
+    return static_cast<i128>(neg ? static_cast<u128>(0) - mag : mag);
+}
+__device__ __forceinline__ i128 cmul_binom(i128 a, long long c, bool& o) {
+    if (c == 1) return a;
+    return cmul(a, static_cast<i128>(c), o);
+}
+// round_to_int<Int128> (int_ops.hpp:103-110): nearbyint, range [-2^127, 2^127)
+__device__ __forceinline__ i128 round_checked128(double x, bool& o) {
+    const double r = rint(x);
+    const bool ok = r >= -0x1p127 && r < 0x1p127;
+    o |= !ok;
+    return ok ? static_cast<i128>(r) : 0;
+}
+static __device__ __noinline__ i128 rint_div128_exact(double a, double b, bool* o) {
+    bool f = false;
+    const i128 v = round_checked128(ddiv(a, b), f);
+    *o |= f;
+    return v;
+}
+// round_to_int<Int128>(a / b) with the quotient rounded as the reference does
+__device__ __forceinline__ i128 rint_div128(double a, double b, double y, bool& o) {
+    const double q = a * y;
+    const double r = rint(q);
+    const double aq = fabs(q);
+    if (aq < 0x1p49 && fabs(q - r) < 0.5 - aq * 0x1p-50) return static_cast<i128>(static_cast<int64_t>(r));
+    return rint_div128_exact(a, b, &o);
+}
+
 }  // namespace dev
 }  // namespace sphray_b200

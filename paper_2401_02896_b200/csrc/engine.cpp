@@ -215,6 +215,7 @@ void Engine::upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_
     CUDA_OK(cudaMemcpyAsync(d_lut_.p, lut.rows.data(), lut.rows.size() * sizeof(double),
                             cudaMemcpyHostToDevice, stream_));
     double extent = 0.0;
+    double center[3] = {0.0, 0.0, 0.0};
     if (n > 0) {
         // The raw particles go up on the aux stream from a helper thread (a
         // pageable copy holds its calling thread) while this thread computes
@@ -259,6 +260,7 @@ void Engine::upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_
             extent = std::sqrt(dx * dx + dy * dy + dz * dz);
             if (!std::isfinite(extent)) extent = 1e300;
             extent += 4.0 * hmax * lut.q;  // knots reach about q h beyond a centre
+            for (int a = 0; a < 3; ++a) center[a] = 0.5 * (lo[a] + hi[a]);
         }
         double inv[3];
         for (int a = 0; a < 3; ++a) {
@@ -284,6 +286,7 @@ void Engine::upload_scene(const sphray_particle* ps, size_t n, const sphray_lut_
     lut_ = std::move(lut);
     n_ = n;
     scene_extent_ = extent;
+    std::copy(center, center + 3, scene_center_);
     shape_key_[0] = -1;  // re-derive the render CTA shape for the new LUT
     has_scene_ = true;
 }
@@ -604,12 +607,23 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     const CamConst C = make_camera(cam);  // render_scene: cam.validate() (raycast.hpp:419)
     validate_tf(tf, ntf);                 // raycast.hpp:420
     if (!has_scene_) fail(SPHRAY_ERR_CONFIG, "no scene uploaded");
-    if (qc.int_width != 64 && qc.int_width != 32)
-        fail(SPHRAY_ERR_CONFIG,
-             "int_width " + std::to_string(qc.int_width) +
-                 ": the B200 path serves render_scene<int32_t> and <int64_t> (128-bit quanta are "
-                 "not supported)");
-    const bool w32 = qc.int_width == 32;
+    if (qc.int_width != 64 && qc.int_width != 32 && qc.int_width != 128)
+        fail(SPHRAY_ERR_CONFIG, "int width must be one of 32, 64, 128");
+    const bool w32 = qc.int_width == 32, w128 = qc.int_width == 128;
+    if (w128) {
+        if (dumps)
+            fail(SPHRAY_ERR_CONFIG, "int_width 128: the validation outputs hold int64 coefficients");
+        // knot positions stay int64 on the device (coefficients and the merge
+        // are 128-bit): every position is within |t| < distance to the scene + extent
+        const double dx = C.pos[0] - scene_center_[0], dy = C.pos[1] - scene_center_[1],
+                     dz = C.pos[2] - scene_center_[2];
+        const double reach = std::sqrt(dx * dx + dy * dy + dz * dz) + scene_extent_;
+        if (!(reach / qc.tau < 0x1p62))
+            fail(SPHRAY_ERR_CAPACITY,
+                 "int_width 128: knot positions beyond int64 (t / tau up to " + std::to_string(reach / qc.tau) +
+                     ") are not supported on the B200 path");
+    }
+    const int jb = w128 ? 16 : 8;  // bytes per jump in the window
     const int D = lut_.D, m = lut_.m;
     const double step = opts.step > 0.0 ? opts.step : ds.h_r / 8.0;  // raycast.hpp:424
     const int W = C.W, H = C.H;
@@ -878,13 +892,14 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     // is a heuristic; rays that still overflow go to the robust retry pass.)
     // int_width 32 frames run the robust variant too (its quantize and merge
     // carry the Checked<int32_t> range tests, render_kernel.cuh / quantize.cuh)
-    const bool robust_frame = scene_extent_ / qc.tau > 2147483648.0 || w32;
+    const bool robust_frame = scene_extent_ / qc.tau > 2147483648.0 || w32 || w128;
     P.robust = robust_frame ? 1 : 0;
+    P.w128 = w128 ? 1 : 0;
     const size_t tfb =
         (tfb_full <= 4096 && !dumps && !robust_frame && !std::getenv("SPHRAY_TF_GLOBAL")) ? tfb_full : 0;
     P.tf_smem = static_cast<int>(tfb);
     auto best_shape = [&](int cap_, int& warps_, int& bps_) {
-        const size_t wb_ = warp_smem_bytes(D, cap_, m);
+        const size_t wb_ = warp_smem_bytes(D, cap_, m, jb);
         int best_ = 0;
         warps_ = 1;
         bps_ = 0;
@@ -905,7 +920,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     int cap = 0, warps = 1, bps = 0;
     // validation dumps (hits / pieces) are written as rays run, so a ray must
     // not be re-run: dump frames use the widest window from the start
-    const long long shape_key[4] = {D * 16 + lut_.K, m, static_cast<long long>(tfb),
+    const long long shape_key[4] = {D * 16 + lut_.K + 1024 * jb, m, static_cast<long long>(tfb),
                                     dumps ? -1 : opts.window};
     if (std::equal(shape_key, shape_key + 4, shape_key_)) {
         cap = shape_val_[0];
@@ -913,11 +928,11 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         bps = shape_val_[2];
     } else if (dumps) {
         cap = 65535;
-        while (cap > 64 && warp_smem_bytes(D, cap, m) + tfb > kSmemLimit) cap = cap * 15 / 16;
+        while (cap > 64 && warp_smem_bytes(D, cap, m, jb) + tfb > kSmemLimit) cap = cap * 15 / 16;
         best_shape(cap, warps, bps);
     } else if (opts.window > 0) {
         cap = std::min(opts.window, 65535);
-        if (warp_smem_bytes(D, cap, m) + tfb > kSmemLimit)
+        if (warp_smem_bytes(D, cap, m, jb) + tfb > kSmemLimit)
             fail(SPHRAY_ERR_CONFIG, "knot window does not fit shared memory");
         best_shape(cap, warps, bps);
     } else {
@@ -937,7 +952,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     shape_val_[0] = cap;
     shape_val_[1] = warps;
     shape_val_[2] = bps;
-    const size_t wb = warp_smem_bytes(D, cap, m);
+    const size_t wb = warp_smem_bytes(D, cap, m, jb);
     if (const char* e = std::getenv("SPHRAY_BPS"))  // diagnostics: fewer CTAs per SM
         bps = std::max(1, std::min(bps, std::atoi(e)));
     if (bps < 1) bps = 1;
@@ -975,7 +990,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
         retry = 0;
     }
     int cap2 = 65535;
-    while (cap2 > cap && warp_smem_bytes(D, cap2, m) + tfb > kSmemLimit) cap2 = cap2 * 15 / 16;
+    while (cap2 > cap && warp_smem_bytes(D, cap2, m, jb) + tfb > kSmemLimit) cap2 = cap2 * 15 / 16;
     if (retry > 0 && cap2 <= cap) {
         defer(SPHRAY_ERR_CAPACITY, "knot window cannot grow");
         retry = 0;
@@ -983,7 +998,7 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     if (retry > 0) {
         FrameParams P2 = P;
         P2.cap = cap2;
-        P2.warp_bytes = static_cast<int>(warp_smem_bytes(D, cap2, m));
+        P2.warp_bytes = static_cast<int>(warp_smem_bytes(D, cap2, m, jb));
         P2.ray_list = d_retry_.as<uint32_t>();
         P2.tf_smem = 0;  // the robust retry variant reads the TF from global memory
         P2.total_work = retry;
@@ -1158,6 +1173,8 @@ void Engine::quantize_hits(const sphray_particle* ps, size_t nhits, const double
                            int64_t* knot_t, int64_t* knot_b, int32_t* knot_count) {
     set_device();
     const LutHost L = make_lut(lutv);
+    if (qc.int_width == 128)
+        fail(SPHRAY_ERR_CONFIG, "int_width 128: quantize_hits returns int64 jumps");
     if (nhits == 0) return;
     const int D = L.D, KN = L.K + 1;
     std::vector<double> powh(nhits * D);

@@ -110,6 +110,7 @@ class Engine {
     bool has_scene_ = false;
     size_t n_ = 0;
     double scene_extent_ = 0.0;  // particle bbox diagonal + 2 max h (window offset range check)
+    double scene_center_[3] = {0.0, 0.0, 0.0};  // particle bbox centre
     LutHost lut_;
     DevBuf d_raw_, d_powh_raw_, d_codes_, d_codes2_, d_idx_, d_idx2_, d_tmp_;
     DevBuf d_pxyzh_, d_mvr_, d_powh_, d_orig_, d_lut_;

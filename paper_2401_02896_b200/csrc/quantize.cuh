@@ -6,6 +6,8 @@
 // Checked<int64_t> semantics: wrapping arithmetic plus an overflow flag.
 #pragma once
 
+#include <type_traits>
+
 #include "device_math.cuh"
 #include "render.cuh"
 
@@ -86,17 +88,32 @@ __device__ __forceinline__ bool quantize_positions(const QuantParams& Q, double 
 // (quantize.hpp:221-222 with the libm parts precomputed on the host),
 // X[2D..3D) = recip_or_nan(X[D..2D)) for rint_div.
 // sink(o, t, b) receives distinct knot o (0..nk) with its D+1 jumps.
-template <int D, int M, bool EVEN, class Sink, bool N32 = false>
+// S: the Checked integer of the jumps -- int64_t, or __int128 for int_width
+// 128 (positions stay int64: the window's positions are int64).
+template <class S>
+__device__ __forceinline__ S rint_div_s(double a, double b, double y, bool& o) {
+    if constexpr (sizeof(S) == 16) return rint_div128(a, b, y, o);
+    else return rint_div(a, b, y, o);
+}
+template <class S>
+__device__ __forceinline__ S narrow_s(S v, bool on, bool& o) {
+    if constexpr (sizeof(S) == 16) return v;
+    else return narrow32(v, on, o);
+}
+
+template <int D, int M, bool EVEN, class Sink, bool N32 = false, class S = int64_t>
 __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double* X,
                                               const HitPositions<M>& hp, bool& ovf,
                                               Sink&& sink) {
+    using U = std::conditional_t<sizeof(S) == 16, unsigned __int128, uint64_t>;
+    constexpr S kMin = static_cast<S>(static_cast<U>(1) << (8 * sizeof(S) - 1));
     const bool n32 = N32 && Q.w32;
-    auto nw = [&](int64_t v) { return narrow32(v, n32, ovf); };
+    auto nw = [&](S v) { return narrow_s<S>(v, n32, ovf); };
     constexpr int m = M;
     constexpr int KN = HitPositions<M>::KN;
     constexpr bool even = EVEN;  // K even (compile time: dead closure code stays out)
-    int64_t negk[M][D + 1];  // negk[k-1] == bneg[m-k] of lut.hpp:106
-    int64_t center[D + 1];
+    S negk[M][D + 1];  // negk[k-1] == bneg[m-k] of lut.hpp:106
+    S center[D + 1];
 #pragma unroll
     for (int k = 0; k < M; ++k)
 #pragma unroll
@@ -115,7 +132,7 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
             } else {
                 ii = c1 + (k - 2) * D + (d - 1);
             }
-            const int64_t bp = nw(rint_div(dmul(X[d - 1], hp.row[m + ii]), X[D + d - 1], X[2 * D + d - 1], ovf));
+            const S bp = nw(rint_div_s<S>(dmul(X[d - 1], hp.row[m + ii]), X[D + d - 1], X[2 * D + d - 1], ovf));
             negk[k - 1][d] = (d & 1) ? bp : nw(cneg(bp, ovf));  // lut.hpp:107-109
         }
     }
@@ -123,14 +140,14 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
         // even K: the centre knot carries the odd-order jumps (lut.hpp:118-130)
 #pragma unroll
         for (int d = 1; d <= D; d += 2) {
-            int64_t acc = 0;
+            S acc = 0;
 #pragma unroll
             for (int k = 1; k <= M; ++k) {
-                const int64_t off = nw(csub(hp.pos[k], hp.pos[0], ovf));
-                int64_t pw = 1;  // off^(j-d), built one step at a time as lut.hpp:123-126
+                const S off = nw(static_cast<S>(csub(hp.pos[k], hp.pos[0], ovf)));
+                S pw = 1;  // off^(j-d), built one step at a time as lut.hpp:123-126
 #pragma unroll
                 for (int j = d; j <= D; ++j) {
-                    int64_t t = nw(cmul_binom(negk[k - 1][j], binom(j, d), ovf));
+                    S t = nw(cmul_binom(negk[k - 1][j], binom(j, d), ovf));
                     if (j > d) t = nw(cmul(t, pw, ovf));  // * 1 at j == d
                     acc = nw(cadd(acc, t, ovf));
                     if (j < D) pw = (j == d) ? off : nw(cmul(pw, off, ovf));
@@ -142,13 +159,13 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
         // odd K: the innermost pair closes, descending odd d (lut.hpp:131-145)
 #pragma unroll
         for (int d = (D % 2 == 1 ? D : D - 1); d >= 1; d -= 2) {
-            int64_t acc = 0;
+            S acc = 0;
 #pragma unroll
             for (int k = 2; k <= M; ++k) acc = nw(cadd(acc, negk[k - 1][d], ovf));
 #pragma unroll
             for (int k = 1; k <= M; ++k) {
-                const int64_t off = nw(csub(hp.pos[k], hp.pos[0], ovf));
-                int64_t pw = off;
+                const S off = nw(static_cast<S>(csub(hp.pos[k], hp.pos[0], ovf)));
+                S pw = off;
 #pragma unroll
                 for (int j = d + 1; j <= D; ++j) {
                     acc = nw(cadd(acc, nw(cmul(nw(cmul_binom(negk[k - 1][j], binom(j, d), ovf)), pw, ovf)), ovf));
@@ -159,26 +176,26 @@ __device__ __forceinline__ void quantize_emit(const QuantParams& Q, const double
         }
     }
     // jumps in emission order (lut.hpp:147-166), static indices like kpos
-    auto jump = [&](int q, int d) -> int64_t {
+    auto jump = [&](int q, int d) -> S {
         if (q < M) return negk[M - 1 - q][d];
         const int j = q - M;  // even: 0 = centre, k = j; odd: k = j + 1
         if (even) {
             if (j == 0) return center[d];
-            const int64_t v = negk[j - 1][d];
-            return (d & 1) ? v : static_cast<int64_t>(0ull - static_cast<uint64_t>(v));
+            const S v = negk[j - 1][d];
+            return (d & 1) ? v : static_cast<S>(static_cast<U>(0) - static_cast<U>(v));
         }
         if (j + 1 > M) return 0;
-        const int64_t v = negk[j][d];
-        return (d & 1) ? v : static_cast<int64_t>(0ull - static_cast<uint64_t>(v));
+        const S v = negk[j][d];
+        return (d & 1) ? v : static_cast<S>(static_cast<U>(0) - static_cast<U>(v));
     };
     // the positive side negates even orders (checked in the reference)
 #pragma unroll
     for (int k = 1; k <= M; ++k)
 #pragma unroll
         for (int d = 0; d <= D; d += 2)
-            ovf |= negk[k - 1][d] == INT64_MIN || (n32 && negk[k - 1][d] == INT32_MIN);
+            ovf |= negk[k - 1][d] == kMin || (n32 && negk[k - 1][d] == INT32_MIN);
     // coincident merge of quantize.hpp:229-242
-    int64_t cur[D + 1];
+    S cur[D + 1];
 #pragma unroll
     for (int d = 0; d <= D; ++d) cur[d] = jump(0, d);
     int o = 0;

@@ -285,9 +285,9 @@ void launch_quantize_hits_t(const QuantParams& Q, const sphray_particle* ps, con
             fail(SPHRAY_ERR_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
     } while (0)
 
-size_t warp_smem_bytes(int D, int cap, int mm) {
+size_t warp_smem_bytes(int D, int cap, int mm, int jb) {
     (void)mm;
-    return warp_bytes_for(D, cap);
+    return warp_bytes_for(D, cap, jb);
 }
 
 // Every (D, m) the reference admits: D in [1,6], m = ceil(K/2) in [1,4]

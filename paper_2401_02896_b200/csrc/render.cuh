@@ -33,11 +33,12 @@ constexpr int kMaxJ = kMaxM * kMaxDegree;
 // Shared-memory bytes of one warp's knot window (layout: render_kernel.cuh carve()).
 SPHRAY_HD inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-SPHRAY_HD inline size_t warp_bytes_for(int D, int cap) {
+// jb: bytes per jump (8; 16 for int_width 128)
+SPHRAY_HD inline size_t warp_bytes_for(int D, int cap, int jb = 8) {
     size_t b = 0;
-    b += align16(sizeof(uint64_t) * D * cap);        // pool: jumps of orders 1..D
-    b += align16(sizeof(uint32_t) * cap);            // pt: position offsets
-    b += align16(sizeof(uint64_t) * (D + 2));         // open piece
+    b += align16(static_cast<size_t>(jb) * D * cap);  // pool: jumps of orders 1..D
+    b += align16((jb == 16 ? 8 : 4) * static_cast<size_t>(cap));  // pt: position offsets
+    b += align16(static_cast<size_t>(jb) * (D + 2));  // open piece
     b += align16(sizeof(double) * kHitQueue * 2);     // hit queue: d2, t_chi
     b += align16(sizeof(int32_t) * kHitQueue);        // hit queue: particle
     b += align16(sizeof(uint16_t) * cap * 2);         // ps, fl (+ flush set)
@@ -91,6 +92,7 @@ struct FrameParams {
     int warp_bytes;  // dynamic smem per warp
     int tf_smem;     // bytes of the per-CTA shared copy of tf after the windows (0: read global)
     int robust;      // use the robust variant (rebasing window offsets) for this launch
+    int w128;        // int_width 128: the robust variant with a modulo-2^128 merge
     // work distribution
     unsigned long long* work_counter;
     uint64_t total_work;
@@ -162,7 +164,7 @@ struct PrepParams {
     int tiles_x, rank, nranks;
 };
 
-size_t warp_smem_bytes(int D, int cap, int m);
+size_t warp_smem_bytes(int D, int cap, int m, int jb = 8);
 int max_blocks_per_sm(int D, int m, int warps, size_t smem, bool even_k);
 // dataset_stats (quantize.hpp:129-165) of the resident scene: medians of
 // mass, density, h, value (med[0..3]), phi_max, and whether some particle has

@@ -124,8 +124,8 @@ __device__ __forceinline__ void tf_sample(const Ld& ld, int n, double v, double&
     const int last = kTfStride * (n - 1);
     const bool lo = v <= ld(0), hi = v >= ld(last);
     int a = 0;
-    if (!lo && !hi) {
-        int i = kTfStride;
+    if (!lo && !hi) {  // the reference's linear search for the bracket (a branch-free
+        int i = kTfStride;  // count measured slower: the loop mostly exits at once)
         while (ld(i) < v) i += kTfStride;
         a = i - kTfStride;
     }
@@ -216,14 +216,53 @@ __device__ __forceinline__ double alpha_of(double x) {
 
 // sphray_piece_mix (include/sphray_gpu.h) of one FieldPiece, for the per-ray
 // piece checksum of sphray_ray_record.
-template <int D>
-__device__ __forceinline__ uint64_t piece_mix(int64_t t, const uint64_t (&a)[D + 1]) {
+// The merge's integer: U = uint64_t (int_width 32 / 64) or unsigned __int128
+// (int_width 128); SOf<U> is its signed twin.
+template <class U>
+using SOf = std::conditional_t<sizeof(U) == 16, __int128, int64_t>;
+
+template <class U>
+__device__ __forceinline__ U shfl_up_u(U v, int o) {
+    if constexpr (sizeof(U) == 16) {
+        const uint64_t lo = __shfl_up_sync(kFull, static_cast<unsigned long long>(v), o);
+        const uint64_t hi = __shfl_up_sync(kFull, static_cast<unsigned long long>(v >> 64), o);
+        return (static_cast<U>(hi) << 64) | lo;
+    } else {
+        return __shfl_up_sync(kFull, static_cast<unsigned long long>(v), o);
+    }
+}
+template <class U>
+__device__ __forceinline__ U shfl_idx_u(U v, int src) {
+    if constexpr (sizeof(U) == 16) {
+        const uint64_t lo = __shfl_sync(kFull, static_cast<unsigned long long>(v), src);
+        const uint64_t hi = __shfl_sync(kFull, static_cast<unsigned long long>(v >> 64), src);
+        return (static_cast<U>(hi) << 64) | lo;
+    } else {
+        return __shfl_sync(kFull, static_cast<unsigned long long>(v), src);
+    }
+}
+template <class U>
+__device__ __forceinline__ U warp_incl_scan_u(U v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const U u = shfl_up_u(v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+template <class U>
+__device__ __forceinline__ double to_double(U a) {
+    return static_cast<double>(static_cast<SOf<U>>(a));
+}
+
+template <int D, class U>
+__device__ __forceinline__ uint64_t piece_mix(int64_t t, const U (&a)[D + 1]) {
     constexpr uint64_t M[8] = {0x9E3779B97F4A7C15ull, 0xC2B2AE3D27D4EB4Full, 0x165667B19E3779F9ull,
                                0x27D4EB2F165667C5ull, 0x94D049BB133111EBull, 0xBF58476D1CE4E5B9ull,
                                0xD6E8FEB86659FD93ull, 0xFF51AFD7ED558CCDull};
     uint64_t x = static_cast<uint64_t>(t) * M[0];
 #pragma unroll
-    for (int d = 0; d <= D; ++d) x += a[d] * M[d + 1];
+    for (int d = 0; d <= D; ++d) x += static_cast<uint64_t>(a[d]) * M[d + 1];  // low 64 bits
     x ^= x >> 31;
     x *= 0xBF58476D1CE4E5B9ull;
     x ^= x >> 29;
@@ -239,10 +278,29 @@ __device__ __forceinline__ uint64_t piece_mix(int64_t t, const uint64_t (&a)[D +
 // left int64 -- the case where render_scene<int64_t> throws OverflowError and
 // a wrapped merge would silently give a wrong field.  A non-finite prediction
 // (astronomic terms) counts as overflow too.
-template <int D>
+template <int D, class U>
 __device__ __forceinline__ bool shift_overflows(const double (&v)[D + 1], double delta,
-                                                const uint64_t (&w)[D + 1]) {
+                                                const U (&w)[D + 1]) {
+    constexpr double kLim = sizeof(U) == 16 ? 0x1p126 : 0x1p62;
     if (!SPHRAY_OVF_CHECK) return false;
+    if (SPHRAY_OVF_CHECK == 3 && sizeof(U) == 8) {
+        // the same prediction in fp32 (relative error ~2^-22 of the terms:
+        // far below the 2^62 margin for any polynomial that stays in range
+        // over the step; a top coefficient is unchanged by a shift)
+        float q[D + 1];
+#pragma unroll
+        for (int d = 0; d <= D; ++d) q[d] = static_cast<float>(v[d]);
+        const float dl = static_cast<float>(delta);
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = D - 1; j >= i; --j) q[j] = fmaf(dl, q[j + 1], q[j]);
+        bool bad = false;
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+            bad |= !(fabsf(q[d] - static_cast<float>(static_cast<int64_t>(w[d]))) < 0x1p62f);
+        return bad;
+    }
     double p[D + 1];
 #pragma unroll
     for (int d = 0; d <= D; ++d) p[d] = v[d];
@@ -253,7 +311,7 @@ __device__ __forceinline__ bool shift_overflows(const double (&v)[D + 1], double
     bool bad = false;
 #pragma unroll
     for (int d = 0; d <= D; ++d)
-        bad |= !(fabs(p[d] - static_cast<double>(static_cast<int64_t>(w[d]))) < 0x1p62);
+        bad |= !(fabs(p[d] - to_double(w[d])) < kLim);
     return bad;
 }
 
@@ -288,17 +346,18 @@ __device__ __forceinline__ bool step_overflows(const uint64_t (&b)[D + 1], uint6
     return shift_overflows<D>(v, static_cast<double>(static_cast<int64_t>(dl)), a);
 }
 
-// a += j modulo 2^64, flagging signed overflow (Checked<int64_t> +, int_ops.hpp:73-80)
-__device__ __forceinline__ uint64_t add_checked(uint64_t a, uint64_t j, bool& o) {
-    const uint64_t r = a + j;
-    if (SPHRAY_OVF_CHECK) o |= static_cast<int64_t>((a ^ r) & (j ^ r)) < 0;
+// a += j modulo 2^64 (2^128), flagging signed overflow (Checked<Int> +, int_ops.hpp:73-80)
+template <class U>
+__device__ __forceinline__ U add_checked(U a, U j, bool& o) {
+    const U r = a + j;
+    if (SPHRAY_OVF_CHECK) o |= static_cast<SOf<U>>((a ^ r) & (j ^ r)) < 0;
     return r;
 }
 
 struct WarpMem {
-    uint32_t* pt;    // cap: position offsets (see the file comment)
-    uint64_t* pool;  // D x cap: jumps of orders 1..D
-    uint64_t* open;  // D+2: the open piece (t, a_0..a_D)
+    void* pt;        // cap: position offsets (u32; u64 for int_width 128, see the file comment)
+    void* pool;      // D x cap: jumps of orders 1..D (the merge's integer, 8 or 16 bytes)
+    void* open;      // D+2: the open piece (t, a_0..a_D)
     double* hq_d2;  // hit queue (candidate order): squared distance of closest approach
     double* hq_t;
     int32_t* hq_p;
@@ -310,16 +369,17 @@ struct WarpMem {
     uint64_t* bar;    //               the mbarrier their bulk copy completes on
 };
 
-__device__ inline WarpMem carve(char* base, int D, int cap) {
-    // layout must match warp_bytes_for (render.cuh)
+__device__ inline WarpMem carve(char* base, int D, int cap, int jb) {
+    // layout must match warp_bytes_for (render.cuh); jb = bytes per jump
+    // (16 also selects 8-byte position offsets)
     WarpMem w;
     char* p = base;
-    w.pool = reinterpret_cast<uint64_t*>(p);
-    p += align16(sizeof(uint64_t) * D * cap);
-    w.pt = reinterpret_cast<uint32_t*>(p);
-    p += align16(sizeof(uint32_t) * cap);
-    w.open = reinterpret_cast<uint64_t*>(p);
-    p += align16(sizeof(uint64_t) * (D + 2));
+    w.pool = p;
+    p += align16(static_cast<size_t>(jb) * D * cap);
+    w.pt = p;
+    p += align16((jb == 16 ? 8 : 4) * static_cast<size_t>(cap));
+    w.open = p;
+    p += align16(static_cast<size_t>(jb) * (D + 2));
     w.hq_d2 = reinterpret_cast<double*>(p);
     w.hq_t = w.hq_d2 + kHitQueue;
     p += align16(sizeof(double) * kHitQueue * 2);
@@ -416,12 +476,13 @@ struct Compositor {
     // by sigma, and the piece-local abscissa x0 + (s + 1/2) dx of sample s.
     // Returns 0 when nothing is sampled (empty interval, or a zero piece
     // under a transfer function that is clear at 0: alpha = 1 - exp(-0) = 0).
-    __device__ __forceinline__ int piece_setup(int64_t ts, int64_t te, const uint64_t (&a)[D + 1],
+    template <class U>
+    __device__ __forceinline__ int piece_setup(int64_t ts, int64_t te, const U (&a)[D + 1],
                                                double (&c)[D + 1], double& x0, double& dx,
                                                double& dt) const {
         double A[D + 1];
 #pragma unroll
-        for (int d = 0; d <= D; ++d) A[d] = static_cast<double>(static_cast<int64_t>(a[d]));
+        for (int d = 0; d <= D; ++d) A[d] = to_double(a[d]);
         return piece_setup_d(ts, te, A, c, x0, dx, dt);
     }
     // the same from the coefficients already converted to double (exact
@@ -450,12 +511,13 @@ struct Compositor {
     }
 
     // Samples one piece into a lane's running (T, colour).
-    __device__ __forceinline__ void composite_piece(int64_t ts, int64_t te, const uint64_t (&a)[D + 1],
+    template <class U>
+    __device__ __forceinline__ void composite_piece(int64_t ts, int64_t te, const U (&a)[D + 1],
                                                     bool stop, double& Tl, double& cr, double& cg,
                                                     double& cb, int& nsmp) const {
         double A[D + 1];
 #pragma unroll
-        for (int d = 0; d <= D; ++d) A[d] = static_cast<double>(static_cast<int64_t>(a[d]));
+        for (int d = 0; d <= D; ++d) A[d] = to_double(a[d]);
         composite_piece_d(ts, te, A, stop, Tl, cr, cg, cb, nsmp);
     }
     __device__ __forceinline__ void composite_piece_d(int64_t ts, int64_t te, const double (&A)[D + 1],
@@ -475,10 +537,10 @@ struct Compositor {
 
 };
 
-template <int D>
+template <int D, class U>
 struct ReplayIn {
-    uint64_t E[D + 1];   // sum of the jumps before the run, around tref
-    uint64_t oa[D + 1];  // the previous open piece (lead lane)
+    U E[D + 1];   // sum of the jumps before the run, around tref
+    U oa[D + 1];  // the previous open piece (lead lane)
     int64_t ot;
     bool lead;
     double Tb;  // the run's true starting transmittance
@@ -491,17 +553,17 @@ struct ReplayOut {
 // of RayWorker::walk from the true T with the per-sample stop test.  Out of
 // line: it runs at most once per ray, and the render kernel is
 // instruction-cache bound.
-template <int D, bool TS>
+template <int D, bool TS, class U, class PT>
 __device__ __noinline__ ReplayOut replay_run(const FrameParams& P, uint32_t tf_sa, const uint16_t* fs,
-                                             const uint32_t* pt, const uint64_t* pool, int cap,
+                                             const PT* pt, const U* pool, int cap,
                                              int64_t tb, int64_t tref, int k0, int k1, int nsel,
-                                             ReplayIn<D> in) {
+                                             ReplayIn<D, U> in) {
     const Compositor<D, TS> cmp{P, tf_sa};
     double Tl = in.Tb, cr = 0.0, cg = 0.0, cb = 0.0;
     int nsmp = 0;
     int64_t tcur = tb + static_cast<int64_t>(pt[fs[k0]]);
     if (in.lead) cmp.composite_piece(in.ot, tcur, in.oa, true, Tl, cr, cg, cb, nsmp);
-    uint64_t Pc[D + 1];
+    U Pc[D + 1];
 #pragma unroll
     for (int d = 0; d <= D; ++d) Pc[d] = in.E[d];
     taylor_shift<D>(Pc, static_cast<uint64_t>(tcur) - static_cast<uint64_t>(tref));
@@ -527,7 +589,7 @@ __device__ __noinline__ ReplayOut replay_run(const FrameParams& P, uint32_t tf_s
 // REC: the per-ray records (piece checksums) are compiled in; the production
 // kernel is instantiated with and without them (the checksum code costs ~2% of
 // the frame even when disabled at run time), the robust variant always has them.
-template <int D, int M, bool TS, bool DUMP, bool EVEN, bool REC>
+template <int D, int M, bool TS, bool DUMP, bool EVEN, bool REC, class U = uint64_t>
 class RayWorker {
    public:
     static constexpr int KN = 2 * M + 1;  // knots per hit, at most
@@ -541,7 +603,14 @@ class RayWorker {
     uint16_t* fs = nullptr;  // flush set of the current flush (w.fl + nfree)
     int64_t tb = 0;          // position base of pt[]
     bool has_base = false;
-    uint64_t G[D + 1];  // running sum of jumps shifted to tref (mod 2^64)
+    using S = SOf<U>;
+    static constexpr bool kW64 = sizeof(U) == 8;
+    // window position offsets from tb: 32 bits (a live window spans < 2^32
+    // quanta), 64 bits for int_width 128 (tiny tau: one particle's knots can
+    // span more than 2^32 quanta)
+    using PT = std::conditional_t<kW64, uint32_t, uint64_t>;
+    static constexpr uint64_t kSpan = kW64 ? 0x100000000ull : 0x8000000000000000ull;
+    U G[D + 1];  // running sum of jumps shifted to tref (mod 2^64, 2^128)
     int64_t tref = 0;
     bool has_ref = false;
     bool has_open = false;  // w.open holds the last piece
@@ -561,11 +630,14 @@ class RayWorker {
     __device__ RayWorker(const FrameParams& p, WarpMem wm, int l, uint32_t t)
         : P(p), w(wm), lane(l), tf_sa(t), cmp{p, t} {}
 
+    __device__ __forceinline__ PT* pt_p() const { return static_cast<PT*>(w.pt); }
     __device__ __forceinline__ int64_t pool_t(int slot) const {
-        return tb + static_cast<int64_t>(w.pt[slot]);
+        return tb + static_cast<int64_t>(pt_p()[slot]);
     }
-    __device__ __forceinline__ uint64_t& pool_c(int d, int slot) const {
-        return w.pool[(d - 1) * P.cap + slot];
+    __device__ __forceinline__ U& pool_c(int d, int slot) const {
+        return static_cast<U*>(w.pool)[(d - 1) * P.cap + slot];
+    }
+    __device__ __forceinline__ U* open_p() const { return static_cast<U*>(w.open);
     }
 
     __device__ void reset() {
@@ -598,8 +670,8 @@ class RayWorker {
     // (or kept as the open piece when it is the set's last).  `lead`: lane 0
     // first composites the previous flush's open piece (ot, oa).  stop: the
     // early-termination replay (absolute T, no side effects).
-    __device__ void walk(int k0, int k1, int nsel, uint64_t (&Pc)[D + 1], bool comp, bool stop,
-                         bool lead, int64_t ot, const uint64_t (&oa)[D + 1], double& Tl, double& cr,
+    __device__ void walk(int k0, int k1, int nsel, U (&Pc)[D + 1], bool comp, bool stop,
+                         bool lead, int64_t ot, const U (&oa)[D + 1], double& Tl, double& cr,
                          double& cg, double& cb, int& npc, int& nsmp) {
         if (k0 >= k1) return;
         int64_t tcur = pool_t(fs[k0]);
@@ -616,12 +688,12 @@ class RayWorker {
             const int64_t t = tn;
             if (t != tcur) {
                 const uint64_t dl = static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur);
-                if (SPHRAY_OVF_CARRY) {
+                if constexpr (SPHRAY_OVF_CARRY != 0) {
                     taylor_shift<D>(Pc, dl);  // every shift follows an emission in this run
                     if (SPHRAY_OVF_CHECK)
                         aovf |= shift_overflows<D>(A, static_cast<double>(static_cast<int64_t>(dl)), Pc);
                 } else {
-                    uint64_t before[D + 1];
+                    U before[D + 1];
 #pragma unroll
                     for (int d = 0; d <= D; ++d) before[d] = Pc[d];
                     taylor_shift<D>(Pc, dl);
@@ -632,7 +704,7 @@ class RayWorker {
 #pragma unroll
             for (int d = 1; d <= D; ++d) {
                 Pc[d] = add_checked(Pc[d], pool_c(d, s), aovf);
-                if constexpr (DUMP) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
+                if constexpr (DUMP && kW64) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
             }
             const bool more = k + 1 < nsel;
             tn = more ? pool_t(fs[k + 1]) : t;
@@ -640,19 +712,19 @@ class RayWorker {
             ++npc;
             if (SPHRAY_OVF_CARRY)
 #pragma unroll
-                for (int d = 0; d <= D; ++d) A[d] = static_cast<double>(static_cast<int64_t>(Pc[d]));
-            if constexpr (DUMP)
+                for (int d = 0; d <= D; ++d) A[d] = to_double(Pc[d]);
+            if constexpr (DUMP && kW64)
 #pragma unroll
                 for (int d = 0; d <= D; ++d) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
             if constexpr (REC)
-                if (P.ray_rec && !stop) csum += piece_mix<D>(t, Pc);
+                if (P.ray_rec && !stop) csum += piece_mix<D, U>(t, Pc);
             if constexpr (DUMP)
                 if (!stop && P.dump_piece_t) dump_piece(t, Pc);
             if (!more) {
                 if (!stop) {
-                    w.open[0] = static_cast<uint64_t>(t);
+                    open_p()[0] = static_cast<U>(static_cast<S>(t));
 #pragma unroll
-                    for (int d = 0; d <= D; ++d) w.open[1 + d] = Pc[d];
+                    for (int d = 0; d <= D; ++d) open_p()[1 + d] = Pc[d];
                 }
             } else if (comp) {
                 if (SPHRAY_OVF_CARRY)
@@ -664,7 +736,8 @@ class RayWorker {
     }
 
     // validation dump of one FieldPiece
-    __device__ __forceinline__ void dump_piece(int64_t t, const uint64_t (&a)[D + 1]) const {
+    // (int_width 128: the low 64 bits of each coefficient)
+    __device__ __forceinline__ void dump_piece(int64_t t, const U (&a)[D + 1]) const {
         const unsigned long long at = atomicAdd(&P.dump_count[1], 1ull);
         if (at < P.dump_cap_pieces) {
             P.dump_piece_ray[at] = ray_id;
@@ -690,41 +763,41 @@ class RayWorker {
             tref = pool_t(fs[0]);
             has_ref = true;
         }
-        uint64_t S[D + 1];
+        U Sg[D + 1];
 #pragma unroll
-        for (int d = 0; d <= D; ++d) S[d] = 0ull;
+        for (int d = 0; d <= D; ++d) Sg[d] = 0;
         for (int k = k0; k < k1; ++k) {
             const int s = fs[k];
-            uint64_t g[D + 1];
-            g[0] = 0ull;  // b_0 == 0 for every knot
+            U g[D + 1];
+            g[0] = 0;  // b_0 == 0 for every knot
 #pragma unroll
             for (int d = 1; d <= D; ++d) g[d] = pool_c(d, s);
             taylor_shift<D>(g, static_cast<uint64_t>(tref) - static_cast<uint64_t>(pool_t(s)));
 #pragma unroll
-            for (int d = 0; d <= D; ++d) S[d] += g[d];
+            for (int d = 0; d <= D; ++d) Sg[d] += g[d];
         }
-        uint64_t E[D + 1];
+        U E[D + 1];
 #pragma unroll
         for (int d = 0; d <= D; ++d) {
-            const uint64_t inc = warp_incl_scan(S[d], lane);
-            E[d] = G[d] + (inc - S[d]);
-            G[d] += __shfl_sync(kFull, inc, 31);
+            const U inc = warp_incl_scan_u(Sg[d], lane);
+            E[d] = G[d] + (inc - Sg[d]);
+            G[d] += shfl_idx_u(inc, 31);
         }
         const bool lead = lane == 0 && has_open;
         int64_t ot = 0;
-        uint64_t oa[D + 1];
+        U oa[D + 1];
 #pragma unroll
-        for (int d = 0; d <= D; ++d) oa[d] = 0ull;
+        for (int d = 0; d <= D; ++d) oa[d] = 0;
         if (lead) {
-            ot = static_cast<int64_t>(w.open[0]);
+            ot = static_cast<int64_t>(open_p()[0]);
 #pragma unroll
-            for (int d = 0; d <= D; ++d) oa[d] = w.open[1 + d];
+            for (int d = 0; d <= D; ++d) oa[d] = open_p()[1 + d];
         }
         __syncwarp();
         const bool comp = !term;
         double Tl = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
         int npc = 0, nsmp = 0;
-        uint64_t Pc[D + 1];
+        U Pc[D + 1];
 #pragma unroll
         for (int d = 0; d <= D; ++d) Pc[d] = E[d];
         walk(k0, k1, nsel, Pc, comp, false, lead, ot, oa, Tl, cr, cg, cb, npc, nsmp);
@@ -739,13 +812,13 @@ class RayWorker {
             double v[D + 1];
 #pragma unroll
             for (int d = 0; d <= D; ++d) {
-                const uint64_t up = __shfl_up_sync(kFull, static_cast<unsigned long long>(Pc[d]), 1);
-                v[d] = static_cast<double>(static_cast<int64_t>(lane == 0 ? oa[d] : up));
+                const U up = shfl_up_u(Pc[d], 1);
+                v[d] = to_double(lane == 0 ? oa[d] : up);
             }
             if (lane == 0) tp = ot;
             if (k0 < k1 && (lane > 0 || lead)) {
                 const int64_t t0 = pool_t(fs[k0]);
-                uint64_t Ps[D + 1];
+                U Ps[D + 1];
 #pragma unroll
                 for (int d = 0; d <= D; ++d) Ps[d] = E[d];
                 taylor_shift<D>(Ps, static_cast<uint64_t>(t0) - static_cast<uint64_t>(tref));
@@ -781,7 +854,7 @@ class RayWorker {
             if (f < 32) {
                 double T2 = Tb;
                 if (lane == f) {
-                    ReplayIn<D> in;
+                    ReplayIn<D, U> in;
 #pragma unroll
                     for (int d = 0; d <= D; ++d) {
                         in.E[d] = E[d];
@@ -790,7 +863,7 @@ class RayWorker {
                     in.ot = ot;
                     in.lead = lead;
                     in.Tb = Tb;
-                    const ReplayOut o = replay_run<D, TS>(P, tf_sa, fs, w.pt, w.pool, P.cap, tb, tref, k0,
+                    const ReplayOut o = replay_run<D, TS, U, PT>(P, tf_sa, fs, pt_p(), static_cast<const U*>(w.pool), P.cap, tb, tref, k0,
                                                           k1, nsel, in);
                     T2 = o.T;
                     Cr += o.r;
@@ -813,7 +886,8 @@ class RayWorker {
     // first pass ranks with shared atomics (its input order is arbitrary);
     // later passes scatter stably, ranks within a round of 32 from match.any
     // (a per-bit ballot version measured 2% slower).
-    __device__ void sort_flush_radix(int nsel, uint32_t tmin, int bits) {
+    __device__ void sort_flush_radix(int nsel, PT tmin, int bits) {
+        const PT* pt = pt_p();
         uint16_t* src = fs;
         uint16_t* dst = w.ps + np;  // free scratch: np + nsel <= cap
 #pragma unroll 1
@@ -824,7 +898,7 @@ class RayWorker {
             __syncwarp();
 #pragma unroll 1
             for (int i = lane; i < nsel; i += 32) {
-                const uint32_t dg = ((w.pt[src[i]] - tmin) >> shift) & 255u;
+                const uint32_t dg = static_cast<uint32_t>((pt[src[i]] - tmin) >> shift) & 255u;
                 atomicAdd(&w.hist[dg], 1u);
             }
             __syncwarp();
@@ -846,7 +920,7 @@ class RayWorker {
 #pragma unroll 1
                 for (int i = lane; i < nsel; i += 32) {
                     const int sl = src[i];
-                    const uint32_t dg = (w.pt[sl] - tmin) & 255u;
+                    const uint32_t dg = static_cast<uint32_t>(pt[sl] - tmin) & 255u;
                     dst[atomicAdd(&w.hist[dg], 1u)] = static_cast<uint16_t>(sl);
                 }
                 __syncwarp();
@@ -860,7 +934,7 @@ class RayWorker {
                 const int i = c0 + lane;
                 const bool valid = i < nsel;
                 const int sl = valid ? src[i] : 0;
-                const uint32_t dg = valid ? ((w.pt[sl] - tmin) >> shift) & 255u : 0u;
+                const uint32_t dg = valid ? static_cast<uint32_t>((pt[sl] - tmin) >> shift) & 255u : 0u;
                 const unsigned peers = __match_any_sync(kFull, valid ? dg : 256u + lane);
                 const unsigned below = peers & lanemask_lt();
                 const uint32_t base = valid ? w.hist[dg] : 0u;
@@ -890,23 +964,22 @@ class RayWorker {
         // ---- select t < F into fs, compact the rest of ps in place
         fs = w.fl + nfree;  // [nfree, nfree + np) is free space above the stack
         int nsel = 0, nkeep = 0;
-        // F as an offset from tb, clamped to [0, 2^32]
+        // F as an offset from tb, clamped to [0, kSpan]
         const uint64_t dF = static_cast<uint64_t>(F) - static_cast<uint64_t>(tb);
-        const uint64_t Fo = all_ ? 0x100000000ull
-                            : (F <= tb ? 0ull : (dF > 0x100000000ull ? 0x100000000ull : dF));
+        const uint64_t Fo = all_ ? kSpan : (F <= tb ? 0ull : (dF > kSpan ? kSpan : dF));
         // Robust variant (DUMP): every knot kept pending (and every later one)
         // is >= F, so the position base moves up to F in this pass and pt[]
         // offsets only span the live window, not the whole ray (small tau,
         // long rays).  The set being flushed keeps the old base until merged.
         const int64_t tb_next = (DUMP && !all_ && F > tb) ? F : tb;
-        const uint32_t keep_shift =
-            (DUMP && Fo > 0 && Fo < 0x100000000ull) ? static_cast<uint32_t>(Fo) : 0u;
-        uint32_t tmin = 0xffffffffu, tmax = 0u;
+        const PT keep_shift = (DUMP && Fo > 0 && Fo < kSpan) ? static_cast<PT>(Fo) : PT(0);
+        PT tmin = ~PT(0), tmax = 0;
+        PT* pt = pt_p();
         for (int c0 = 0; c0 < np; c0 += 32) {
             const int i = c0 + lane;
             const bool valid = i < np;
             const int s = valid ? w.ps[i] : 0;
-            const uint32_t t = valid ? w.pt[s] : 0u;
+            const PT t = valid ? pt[s] : PT(0);
             const bool sel = valid && static_cast<uint64_t>(t) < Fo;
             const unsigned msel = __ballot_sync(kFull, sel);
             const unsigned mkeep = __ballot_sync(kFull, valid && !sel);
@@ -917,7 +990,7 @@ class RayWorker {
                 tmax = t > tmax ? t : tmax;
             } else if (valid) {
                 w.ps[nkeep + __popc(mkeep & lanemask_lt())] = static_cast<uint16_t>(s);
-                if (keep_shift) w.pt[s] = t - keep_shift;
+                if (keep_shift) pt[s] = t - keep_shift;
             }
             nsel += __popc(msel);
             nkeep += __popc(mkeep);
@@ -932,10 +1005,23 @@ class RayWorker {
             tb = tb_next;
             return;
         }
-        tmin = __reduce_min_sync(kFull, tmin);
-        tmax = __reduce_max_sync(kFull, tmax);
-        const uint32_t range = tmax - tmin;
-        const int bits = range == 0 ? 0 : 32 - __clz(static_cast<int>(range));
+        int bits;
+        if constexpr (kW64) {
+            tmin = __reduce_min_sync(kFull, tmin);
+            tmax = __reduce_max_sync(kFull, tmax);
+            const uint32_t range = tmax - tmin;
+            bits = range == 0 ? 0 : 32 - __clz(static_cast<int>(range));
+        } else {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const PT a = __shfl_xor_sync(kFull, static_cast<unsigned long long>(tmin), o);
+                const PT b = __shfl_xor_sync(kFull, static_cast<unsigned long long>(tmax), o);
+                tmin = a < tmin ? a : tmin;
+                tmax = b > tmax ? b : tmax;
+            }
+            const PT range = tmax - tmin;
+            bits = range == 0 ? 0 : 64 - __clzll(static_cast<long long>(range));
+        }
         if (SPHRAY_KSTATS) {
             const int bb = bits <= 8 ? 0 : bits <= 10 ? 1 : bits <= 12 ? 2 : bits <= 14 ? 3 : bits <= 16 ? 4 : 5;
             SPHRAY_KS(kStatBits0 + bb, 1);
@@ -991,17 +1077,17 @@ class RayWorker {
             const double* xs = P.xy + static_cast<size_t>(pi) * (3 * D);
 #pragma unroll
             for (int d = 0; d < 3 * D; ++d) X[d] = xs[d];
-            auto sink = [&](int o, int64_t t, const int64_t (&b)[D + 1]) {
+            auto sink = [&](int o, int64_t t, const S (&b)[D + 1]) {
                 const int slot = w.fl[slot0 + o];
                 // b[0] is structurally zero (lut.hpp:107-166): only orders 1..D are stored
                 const uint64_t to = static_cast<uint64_t>(t) - static_cast<uint64_t>(tb);
-                far_ |= t < tb || to > 0xffffffffull;
-                w.pt[slot] = static_cast<uint32_t>(to);
+                far_ |= t < tb || (kW64 && to > 0xffffffffull);
+                pt_p()[slot] = static_cast<PT>(to);
 #pragma unroll
-                for (int d = 1; d <= D; ++d) pool_c(d, slot) = static_cast<uint64_t>(b[d]);
+                for (int d = 1; d <= D; ++d) pool_c(d, slot) = static_cast<U>(b[d]);
                 w.ps[np + off + o] = static_cast<uint16_t>(slot);
             };
-            quantize_emit<D, M, EVEN, decltype(sink)&, DUMP>(P.Q, X, hp, ovf, sink);
+            quantize_emit<D, M, EVEN, decltype(sink)&, DUMP, S>(P.Q, X, hp, ovf, sink);
             if (ovf) report_overflow(pi);
         }
         // a ray spanning more than 2^32 position quanta does not fit the
@@ -1209,7 +1295,7 @@ class RayWorker {
             bool residual = false;  // raycast.hpp:477-480: trailing piece must be zero
             if (knots > 0 && complete && has_open) {
 #pragma unroll
-                for (int d = 0; d <= D; ++d) residual |= w.open[1 + d] != 0;
+                for (int d = 0; d <= D; ++d) residual |= open_p()[1 + d] != 0;
             }
             // RayAccumulator op count for P distinct positions (raycast.hpp:217-244)
             const unsigned long long Pp = pieces;
@@ -1245,12 +1331,14 @@ class RayWorker {
     }
 };
 
-template <int D, int M, bool TS, bool DUMP, bool EVEN, bool REC>
+// W128: the merge runs modulo 2^128 (int_width 128; robust variant only)
+template <int D, int M, bool TS, bool DUMP, bool EVEN, bool REC, bool W128 = false>
 __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const __grid_constant__ FrameParams P) {
+    using U = std::conditional_t<W128, unsigned __int128, uint64_t>;
     extern __shared__ __align__(16) char smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const WarpMem wm = carve(smem + static_cast<size_t>(warp) * P.warp_bytes, D, P.cap);
+    const WarpMem wm = carve(smem + static_cast<size_t>(warp) * P.warp_bytes, D, P.cap, static_cast<int>(sizeof(U)));
     uint32_t tf_sa = 0;
     if constexpr (TS) {
         double* st = reinterpret_cast<double*>(smem + static_cast<size_t>(blockDim.x >> 5) * P.warp_bytes);
@@ -1258,7 +1346,7 @@ __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const __grid_constant_
         __syncthreads();
         tf_sa = static_cast<uint32_t>(__cvta_generic_to_shared(st));
     }
-    RayWorker<D, M, TS, DUMP, EVEN, REC> rw(P, wm, lane, tf_sa);
+    RayWorker<D, M, TS, DUMP, EVEN, REC, U> rw(P, wm, lane, tf_sa);
     if (SPHRAY_STAGE && lane == 0) mbar_init(smem_addr(wm.bar));
     __syncwarp();
     while (true) {
@@ -1366,7 +1454,8 @@ void launch_render_tt(const FrameParams& P, int blocks, int warps, cudaStream_t 
     // the production kernel carries none of it (it is instruction-cache
     // sensitive).  The robust variant reads the transfer function from global.
     const bool robust = P.dump_hit_ray || P.dump_piece_t || P.ray_list || P.robust;
-    auto kern = robust ? rk::k_render_rays<D, M, false, true, EVEN, true>
+    auto kern = P.w128 ? rk::k_render_rays<D, M, false, true, EVEN, true, true>
+                : robust ? rk::k_render_rays<D, M, false, true, EVEN, true>
                 : P.tf_smem ? (P.ray_rec ? rk::k_render_rays<D, M, true, false, EVEN, true>
                                          : rk::k_render_rays<D, M, true, false, EVEN, false>)
                             : rk::k_render_rays<D, M, false, false, EVEN, true>;

@@ -192,10 +192,55 @@ def test_int32_distant_particle_overflows_but_int64_renders(ctx, tmp_path):
         assert getattr(st, k) == rst[k], k
 
 
-def test_int128_is_a_config_error(ctx):
-    ps = H.random_cloud(H.MT19937_64(31337), 20, 1.6, -1.2, 1.2)
-    lut = S.load_lut(H.lut_path(4, 3, 16))
+# --------------------------------------------------------------------------- int_width 128
+# render_scene<Int128> on w128 quanta: 128-bit jumps and a modulo-2^128 merge
+# (robust kernel variant); knot positions stay int64.
+
+@pytest.mark.parametrize("case", ["render_test", "blob"])
+def test_int128_renders_match_reference(ctx, case):
+    if case == "blob":
+        ps, ck, tf, lp = ref.generate_scene(1, 3000), H.synth_camera_kwargs(48, 48), H.SYNTH_TF, \
+            H.lut_path(4, 3, 1024)
+    else:
+        ps = H.random_cloud(H.MT19937_64(31337), 120, 1.6, -1.2, 1.2)
+        ck, tf, lp = H.render_test_camera_kwargs(), H.TEST_TF, H.lut_path(4, 3, 16)
+    lut, rl = S.load_lut(lp), ref.Lut(lp)
     ds = S.dataset_stats(ps, lut)
-    with pytest.raises(S.ConfigError):
-        S.render_scene(ps, S.Camera(**H.render_test_camera_kwargs()), S.TransferFunction.from_array(H.TEST_TF),
-                       lut, S.choose_quanta(lut, ds, 128), ds, ctx=ctx)
+    qc = S.choose_quanta(lut, ds, 128)
+    rds = ref.dataset_stats(ps, rl)
+    rqc = ref.choose_quanta(rl, rds, 128)
+    assert (qc.tau, qc.sigma, qc.width) == (rqc.tau, rqc.sigma, 128)
+    rgb, rst, _ = ref.render(ps, ref.Camera(**ck), tf, rl, rqc, rds, accum_bits=128)
+    img, st = S.render_scene(ps, S.Camera(**ck), S.TransferFunction.from_array(tf), lut, qc, ds,
+                             S.RenderOptions(mode=S.MODE_EXACT), ctx=ctx)
+    assert np.abs(img.pixels - rgb).max() <= 1e-4
+    for k in ("knots", "rays_touched", "int_ops", "residual_failures", "skipped_particles"):
+        assert getattr(st, k) == rst[k], k
+    # per-ray FieldPiece checksums (low 64 bits of the 128-bit coefficients)
+    ctx.upload(ps, lut)
+    ctx.set_region(0, 0, 0, 0, record=True)
+    try:
+        ctx.render(S.Camera(**ck), S.TransferFunction.from_array(tf), qc, ds, S.RenderOptions(mode=S.MODE_EXACT))
+        rec = ctx.ray_records()
+    finally:
+        ctx.set_region()
+    _, rrec, _, _, bits = ref.render_region(ps, ref.Camera(**ck), tf, rl, rqc, st.step, 0, 0, ck["width"],
+                                            ck["height"])
+    assert bits == 128
+    for k in ("knots", "pieces", "hits", "piece_checksum"):
+        np.testing.assert_array_equal(rec[k], rrec[k])
+
+
+def test_int128_positions_beyond_int64_fail_loudly(ctx):
+    """Degree-1 tables at 128 bits quantize positions below 1e-19: t / tau leaves
+    int64, which the device's window does not represent (CapacityError, never
+    a wrong image)."""
+    ps = ref.generate_scene(1, 500)
+    lp = H.lut_path(2, 1, 1024)
+    lut = S.load_lut(lp)
+    ds = S.dataset_stats(ps, lut)
+    qc = S.choose_quanta(lut, ds, 128)
+    assert qc.tau < 1e-18
+    with pytest.raises(S.CapacityError):
+        S.render_scene(ps, S.Camera(**H.synth_camera_kwargs(16, 16)), S.TransferFunction.from_array(H.SYNTH_TF),
+                       lut, qc, ds, ctx=ctx)
