@@ -158,6 +158,9 @@ __device__ __forceinline__ int sample_count(double len, double step, double inv_
 #ifndef SPHRAY_ALPHA_MODE
 #define SPHRAY_ALPHA_MODE 2  // 2: series to x^6 below 1/16, fp64 exp above; 0: series to x^8; 1: round-1 fp32 (diagnostics)
 #endif
+#ifndef SPHRAY_WALK_PF
+#define SPHRAY_WALK_PF 1  // walk: shared-memory loads of the next knot issued before the shift
+#endif
 #ifndef SPHRAY_OVF_CARRY
 #define SPHRAY_OVF_CARRY 1  // the walk keeps the last piece as doubles (shared by the overflow test and compositing)
 #endif
@@ -686,6 +689,16 @@ class RayWorker {
         for (int k = k0; k < k1; ++k) {
             const int s = fs[k];
             const int64_t t = tn;
+            const bool more = k + 1 < nsel;
+            // the next knot's position and this knot's jumps are loaded before
+            // the shift (SPHRAY_WALK_PF): their shared-memory latency overlaps it
+            int64_t tnext = t;
+            U jmp[D + 1];
+            if (SPHRAY_WALK_PF) {
+                tnext = more ? pool_t(fs[k + 1]) : t;
+#pragma unroll
+                for (int d = 1; d <= D; ++d) jmp[d] = pool_c(d, s);
+            }
             if (t != tcur) {
                 const uint64_t dl = static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur);
                 if constexpr (SPHRAY_OVF_CARRY != 0) {
@@ -703,11 +716,10 @@ class RayWorker {
             }
 #pragma unroll
             for (int d = 1; d <= D; ++d) {
-                Pc[d] = add_checked(Pc[d], pool_c(d, s), aovf);
+                Pc[d] = add_checked(Pc[d], SPHRAY_WALK_PF ? jmp[d] : pool_c(d, s), aovf);
                 if constexpr (DUMP && kW64) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
             }
-            const bool more = k + 1 < nsel;
-            tn = more ? pool_t(fs[k + 1]) : t;
+            tn = SPHRAY_WALK_PF ? tnext : (more ? pool_t(fs[k + 1]) : t);
             if (more && tn == t) continue;  // more jumps at this position
             ++npc;
             if (SPHRAY_OVF_CARRY)

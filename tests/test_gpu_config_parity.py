@@ -6,7 +6,9 @@
   exact, the full hit set bit-exact (digest), and per ray -- from the
   PRODUCTION render kernel, not the validation-dump variant -- knots, pieces,
   hits, the residual flag and a checksum of the ray's merged FieldPieces.
-* config 3 (16M clustered particles, 2048^2 -- the benchmarked workload):
+* configs 2 (1M blob, 1024^2) and 4 (4M blob, 1024^2, the order sweep's K/D
+  tables incl. degree 1, whose tiny tau takes the robust window variant) and
+  config 3 (16M clustered particles, 2048^2 -- the benchmarked workload):
   pixel regions of the full frame against oracle/_ref run live on this host
   (the reference's own footprint / quantize / sort / accumulate / composite
   on the same camera, restricted to the region's rays): hits bit-exact,
@@ -167,3 +169,42 @@ def test_config3_region_render(c3, region, mode):
         complete = (rec["flags"] & S.RAY_TERMINATED) == 0
     records_equal(rec, rrec["piece_checksum"], rrec["knots"], rrec["pieces"], rrec["hits"],
                   rrec["flags"], complete)
+
+
+# --------------------------------------------------------------------------- configs 2 and 4
+def _blob_case(config, K, D):
+    ps = S.generate_scene(config)
+    lut_path = H.lut_path(K, D, 1024)
+    lut, rl = S.load_lut(lut_path), ref.Lut(lut_path)
+    ds = S.dataset_stats(ps, lut)
+    qc = S.choose_quanta(lut, ds)
+    rds = ref.dataset_stats(ps, rl)
+    rqc = ref.choose_quanta(rl, rds)
+    assert (qc.tau, qc.sigma, ds.h_r) == (rqc.tau, rqc.sigma, rds.h_r)
+    return ps, lut, rl, ds, qc, rqc
+
+
+@pytest.mark.parametrize("config,K,D,region", [(2, 4, 3, (448, 510, 128, 4)), (4, 4, 1, (500, 300, 64, 2)),
+                                               (4, 2, 3, (256, 512, 64, 2))])
+def test_blob_config_region(config, K, D, region):
+    ps, lut, rl, ds, qc, rqc = _blob_case(config, K, D)
+    ck = H.synth_camera_kwargs(1024, 1024)
+    x0, y0, w, h = region
+    with S.Context(0) as ctx:
+        ctx.upload(ps, lut)
+        ctx.set_region(*region, record=True)
+        img, st = ctx.render(S.Camera(**ck), S.TransferFunction.from_array(H.SYNTH_TF), qc, ds,
+                             S.RenderOptions(mode=S.MODE_EXACT))
+        rec = ctx.ray_records()
+        ctx.set_region(*region)
+        p = ctx.pieces(S.Camera(**ck), qc)
+    rgb, rrec, rst, _, _ = ref.render_region(ps, ref.Camera(**ck), H.SYNTH_TF, rl, rqc, st.step, *region)
+    assert float(np.abs(img.pixels[:, x0:x0 + w] - rgb[:, x0:x0 + w]).max()) <= RGB_TOL
+    for k in ("knots", "rays_touched", "int_ops", "residual_failures"):
+        assert getattr(st, k) == rst[k], (k, getattr(st, k), rst[k])
+    records_equal(rec, rrec["piece_checksum"], rrec["knots"], rrec["pieces"], rrec["hits"], rrec["flags"],
+                  np.ones(len(rec), bool))
+    r = ref.pipeline(ps, ref.Camera(**ck), rl, rqc, region=region)
+    np.testing.assert_array_equal(p["rays"], r["rays"])
+    np.testing.assert_array_equal(p["piece_t"], r["piece_t"])
+    np.testing.assert_array_equal(p["piece_a"], r["piece_a"])
