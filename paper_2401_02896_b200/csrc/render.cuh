@@ -10,7 +10,10 @@
 
 namespace sphray_b200 {
 
-constexpr int kTileShift = 3;  // 8x8-pixel screen tiles
+#ifndef SPHRAY_TILE_SHIFT
+#define SPHRAY_TILE_SHIFT 3
+#endif
+constexpr int kTileShift = SPHRAY_TILE_SHIFT;  // 8x8-pixel screen tiles (2: 4x4)
 constexpr int kTile = 1 << kTileShift;
 constexpr int kTileRays = kTile * kTile;
 constexpr int kHitQueue = 64;

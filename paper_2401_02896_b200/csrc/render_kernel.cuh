@@ -158,14 +158,8 @@ __device__ __forceinline__ int sample_count(double len, double step, double inv_
 #ifndef SPHRAY_ALPHA_MODE
 #define SPHRAY_ALPHA_MODE 2  // 2: series to x^6 below 1/16, fp64 exp above; 0: series to x^8; 1: round-1 fp32 (diagnostics)
 #endif
-#ifndef SPHRAY_WALK_PF
-#define SPHRAY_WALK_PF 1  // walk: shared-memory loads of the next knot issued before the shift
-#endif
-#ifndef SPHRAY_OVF_CARRY
-#define SPHRAY_OVF_CARRY 1  // the walk keeps the last piece as doubles (shared by the overflow test and compositing)
-#endif
 #ifndef SPHRAY_OVF_CHECK
-#define SPHRAY_OVF_CHECK 1  // genuine-overflow test of the merge: 1 fp64, 2 fp32 high words + fp64 for long steps (measured slower), 0 off (diagnostics)
+#define SPHRAY_OVF_CHECK 1  // genuine-overflow test of the merge (0: off, diagnostics only)
 #endif
 #ifndef SPHRAY_COLD_OUTLINE
 #define SPHRAY_COLD_OUTLINE 0  // rarely executed code out of line (the kernel is instruction-cache bound)
@@ -286,24 +280,6 @@ __device__ __forceinline__ bool shift_overflows(const double (&v)[D + 1], double
                                                 const U (&w)[D + 1]) {
     constexpr double kLim = sizeof(U) == 16 ? 0x1p126 : 0x1p62;
     if (!SPHRAY_OVF_CHECK) return false;
-    if (SPHRAY_OVF_CHECK == 3 && sizeof(U) == 8) {
-        // the same prediction in fp32 (relative error ~2^-22 of the terms:
-        // far below the 2^62 margin for any polynomial that stays in range
-        // over the step; a top coefficient is unchanged by a shift)
-        float q[D + 1];
-#pragma unroll
-        for (int d = 0; d <= D; ++d) q[d] = static_cast<float>(v[d]);
-        const float dl = static_cast<float>(delta);
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-#pragma unroll
-            for (int j = D - 1; j >= i; --j) q[j] = fmaf(dl, q[j + 1], q[j]);
-        bool bad = false;
-#pragma unroll
-        for (int d = 0; d < D; ++d)
-            bad |= !(fabsf(q[d] - static_cast<float>(static_cast<int64_t>(w[d]))) < 0x1p62f);
-        return bad;
-    }
     double p[D + 1];
 #pragma unroll
     for (int d = 0; d <= D; ++d) p[d] = v[d];
@@ -316,37 +292,6 @@ __device__ __forceinline__ bool shift_overflows(const double (&v)[D + 1], double
     for (int d = 0; d <= D; ++d)
         bad |= !(fabs(p[d] - to_double(w[d])) < kLim);
     return bad;
-}
-
-// The same test for one walk step, from the wrapped coefficients before (b)
-// and after (a) the shift.  Steps of fewer than 256 quanta (the common case)
-// run it in fp32 on the high 32-bit words (units of 2^32): truncating the low
-// words costs < 1 unit, amplified at most (1 + delta)^D < 2^24 units by the
-// shift, far below the 2^30-unit (2^62) threshold an overflow (a difference
-// of k 2^32 units) must cross; longer steps take the fp64 form.
-template <int D>
-__device__ __forceinline__ bool step_overflows(const uint64_t (&b)[D + 1], uint64_t dl,
-                                               const uint64_t (&a)[D + 1]) {
-    if (!SPHRAY_OVF_CHECK) return false;
-    if (SPHRAY_OVF_CHECK == 2 && dl < 256) {
-        float p[D + 1];
-#pragma unroll
-        for (int d = 0; d <= D; ++d) p[d] = static_cast<float>(static_cast<int32_t>(b[d] >> 32));
-        const float dd = static_cast<float>(static_cast<uint32_t>(dl));
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-#pragma unroll
-            for (int j = D - 1; j >= i; --j) p[j] = fmaf(dd, p[j + 1], p[j]);
-        bool bad = false;
-#pragma unroll
-        for (int d = 0; d < D; ++d)  // a_D is unchanged by a shift
-            bad |= !(fabsf(p[d] - static_cast<float>(static_cast<int32_t>(a[d] >> 32))) < 0x1p30f);
-        return bad;
-    }
-    double v[D + 1];
-#pragma unroll
-    for (int d = 0; d <= D; ++d) v[d] = static_cast<double>(static_cast<int64_t>(b[d]));
-    return shift_overflows<D>(v, static_cast<double>(static_cast<int64_t>(dl)), a);
 }
 
 // a += j modulo 2^64 (2^128), flagging signed overflow (Checked<Int> +, int_ops.hpp:73-80)
@@ -678,72 +623,67 @@ class RayWorker {
                          double& cg, double& cb, int& npc, int& nsmp) {
         if (k0 >= k1) return;
         int64_t tcur = pool_t(fs[k0]);
-        if (lead && comp) cmp.composite_piece(ot, tcur, oa, stop, Tl, cr, cg, cb, nsmp);
+        // One compositing site (the kernel is instruction-cache bound): the
+        // previous flush's open piece (lead lane) goes through the same call as
+        // the pieces of the run, in a virtual iteration before the first knot.
+        bool go = lead && comp;
+        int64_t cs = ot, ce = tcur;
         taylor_shift<D>(Pc, static_cast<uint64_t>(tcur) - static_cast<uint64_t>(tref));
         int64_t tn = tcur;
         // the last emitted piece's coefficients as doubles: the overflow test's
         // input for the next shift and the compositing input (one conversion)
         double A[D + 1];
 #pragma unroll
-        for (int d = 0; d <= D; ++d) A[d] = 0.0;
-        for (int k = k0; k < k1; ++k) {
-            const int s = fs[k];
-            const int64_t t = tn;
-            const bool more = k + 1 < nsel;
-            // the next knot's position and this knot's jumps are loaded before
-            // the shift (SPHRAY_WALK_PF): their shared-memory latency overlaps it
-            int64_t tnext = t;
-            U jmp[D + 1];
-            if (SPHRAY_WALK_PF) {
-                tnext = more ? pool_t(fs[k + 1]) : t;
+        for (int d = 0; d <= D; ++d) A[d] = go ? to_double(oa[d]) : 0.0;
+        for (int k = go ? k0 - 1 : k0; k < k1; ++k) {
+            if (k >= k0) {
+                go = false;
+                const int s = fs[k];
+                const int64_t t = tn;
+                const bool more = k + 1 < nsel;
+                // the next knot's position and this knot's jumps are loaded
+                // before the shift: their shared-memory latency overlaps it
+                const int64_t tnext = more ? pool_t(fs[k + 1]) : t;
+                U jmp[D + 1];
 #pragma unroll
                 for (int d = 1; d <= D; ++d) jmp[d] = pool_c(d, s);
-            }
-            if (t != tcur) {
-                const uint64_t dl = static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur);
-                if constexpr (SPHRAY_OVF_CARRY != 0) {
+                if (t != tcur) {
+                    const uint64_t dl = static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur);
                     taylor_shift<D>(Pc, dl);  // every shift follows an emission in this run
                     if (SPHRAY_OVF_CHECK)
                         aovf |= shift_overflows<D>(A, static_cast<double>(static_cast<int64_t>(dl)), Pc);
-                } else {
-                    U before[D + 1];
-#pragma unroll
-                    for (int d = 0; d <= D; ++d) before[d] = Pc[d];
-                    taylor_shift<D>(Pc, dl);
-                    aovf |= step_overflows<D>(before, dl, Pc);
+                    tcur = t;
                 }
-                tcur = t;
-            }
 #pragma unroll
-            for (int d = 1; d <= D; ++d) {
-                Pc[d] = add_checked(Pc[d], SPHRAY_WALK_PF ? jmp[d] : pool_c(d, s), aovf);
-                if constexpr (DUMP && kW64) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
-            }
-            tn = SPHRAY_WALK_PF ? tnext : (more ? pool_t(fs[k + 1]) : t);
-            if (more && tn == t) continue;  // more jumps at this position
-            ++npc;
-            if (SPHRAY_OVF_CARRY)
+                for (int d = 1; d <= D; ++d) {
+                    Pc[d] = add_checked(Pc[d], jmp[d], aovf);
+                    if constexpr (DUMP && kW64) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
+                }
+                tn = tnext;
+                if (more && tn == t) continue;  // more jumps at this position
+                ++npc;
 #pragma unroll
                 for (int d = 0; d <= D; ++d) A[d] = to_double(Pc[d]);
-            if constexpr (DUMP && kW64)
+                if constexpr (DUMP && kW64)
 #pragma unroll
-                for (int d = 0; d <= D; ++d) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
-            if constexpr (REC)
-                if (P.ray_rec && !stop) csum += piece_mix<D, U>(t, Pc);
-            if constexpr (DUMP)
-                if (!stop && P.dump_piece_t) dump_piece(t, Pc);
-            if (!more) {
-                if (!stop) {
-                    open_p()[0] = static_cast<U>(static_cast<S>(t));
+                    for (int d = 0; d <= D; ++d) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
+                if constexpr (REC)
+                    if (P.ray_rec && !stop) csum += piece_mix<D, U>(t, Pc);
+                if constexpr (DUMP)
+                    if (!stop && P.dump_piece_t) dump_piece(t, Pc);
+                if (!more) {
+                    if (!stop) {
+                        open_p()[0] = static_cast<U>(static_cast<S>(t));
 #pragma unroll
-                    for (int d = 0; d <= D; ++d) open_p()[1 + d] = Pc[d];
+                        for (int d = 0; d <= D; ++d) open_p()[1 + d] = Pc[d];
+                    }
+                } else if (comp) {
+                    go = true;
+                    cs = t;
+                    ce = tn;
                 }
-            } else if (comp) {
-                if (SPHRAY_OVF_CARRY)
-                    cmp.composite_piece_d(t, tn, A, stop, Tl, cr, cg, cb, nsmp);
-                else
-                    cmp.composite_piece(t, tn, Pc, stop, Tl, cr, cg, cb, nsmp);
             }
+            if (go) cmp.composite_piece_d(cs, ce, A, stop, Tl, cr, cg, cb, nsmp);
         }
     }
 

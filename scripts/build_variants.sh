@@ -6,6 +6,6 @@ ROOT=$(cd "$(dirname "$0")/.." && pwd)
 while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
   make -s -C "$ROOT/paper_2401_02896_b200/csrc" -j16 OUT="$ROOT/build_variants/lib$name.so" \
-       OBJ="$ROOT/build_variants/obj_$name" EXTRA_NVFLAGS="-DSPHRAY_FAST_BUILD $flags" >/dev/null
+       OBJ="$ROOT/build_variants/obj_$name" EXTRA_NVFLAGS="-DSPHRAY_FAST_BUILD $flags" EXTRA_CXXFLAGS="$flags" >/dev/null
   echo "built build_variants/lib$name.so ($flags)"
 done

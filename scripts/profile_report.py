@@ -105,6 +105,10 @@ def main():
         st = [(fnum(d, k), k.replace("smsp__pcsamp_warps_issue_stalled_", "")) for k in d
               if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")]
         st = [(v, k) for v, k in st if v]
+        if not st:  # no PC sampling in the capture: the WarpStateStats averages
+            pre, suf = "smsp__average_warp_latency_issue_stalled_", ".ratio"
+            st = [(fnum(d, k), k[len(pre):-len(suf)]) for k in d if k.startswith(pre) and k.endswith(suf)]
+            st = [(v, k) for v, k in st if v and not k.endswith("not_issued")]
         tot = sum(v for v, _ in st)
         md += ["", "## Stall reasons (PC sampling)", "", "| reason | share |", "|---|---|"]
         for v, k in sorted(st, reverse=True)[:10]:
