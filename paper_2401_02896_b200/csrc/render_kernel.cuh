@@ -41,6 +41,9 @@
         if (SPHRAY_KSTATS && lane == 0)                                              \
             atomicAdd(&P.stats[idx], static_cast<unsigned long long>(v));            \
     } while (0)
+#ifndef SPHRAY_COLD_OUTLINE
+#define SPHRAY_COLD_OUTLINE 1  // rarely executed code out of line (the kernel is instruction-cache bound)
+#endif
 #ifndef SPHRAY_MAXNREG
 #define SPHRAY_MAXNREG 168
 #endif
@@ -142,9 +145,15 @@ __device__ __forceinline__ void tf_sample(const Ld& ld, int n, double v, double&
 // n = max(2, ceil((hi - lo) / step)) exactly as the reference counts samples
 // (raycast.hpp:367): a multiply by 1/step, with the exact division only when
 // the quotient is within rounding distance of an integer.
+static __device__ __noinline__ int sample_count_long(double len, double step, double q) {
+    double c = ceil(q);
+    if (fabs(q - rint(q)) <= 1e-12 * q + 1e-300) c = ceil(div_exact(len, step));
+    return c > 2.0 ? static_cast<int>(c) : 2;
+}
 __device__ __forceinline__ int sample_count(double len, double step, double inv_step) {
     const double q = len * inv_step;
     if (q < 1.9) return 2;  // len/step < 2 for sure: the common case
+    if (SPHRAY_COLD_OUTLINE) return sample_count_long(len, step, q);
     double c = ceil(q);
     if (fabs(q - rint(q)) <= 1e-12 * q + 1e-300) c = ceil(div_exact(len, step));
     return c > 2.0 ? static_cast<int>(c) : 2;
@@ -156,50 +165,18 @@ __device__ __forceinline__ int sample_count(double len, double step, double inv_
 // glibc's).  Either way alpha is within a few ulps of the reference's, so the
 // early-termination test T <= 1e-3 sees the same transmittance to ~1e-15.
 #ifndef SPHRAY_ALPHA_MODE
-#define SPHRAY_ALPHA_MODE 2  // 2: series to x^6 below 1/16, fp64 exp above; 0: series to x^8; 1: round-1 fp32 (diagnostics)
+#define SPHRAY_ALPHA_MODE 0  // 0: fp64 (series + exp); 1: round-1 fp32 (diagnostics)
 #endif
 #ifndef SPHRAY_OVF_CHECK
 #define SPHRAY_OVF_CHECK 1  // genuine-overflow test of the merge (0: off, diagnostics only)
 #endif
-#ifndef SPHRAY_COLD_OUTLINE
-#define SPHRAY_COLD_OUTLINE 0  // rarely executed code out of line (the kernel is instruction-cache bound)
-#endif
-// 1 - exp(-x) for x >= 1/16: CUDA's fp64 exp is several hundred SASS
-// instructions; out of line it stays out of the hot loop's instruction cache.
-static __device__ __noinline__ double one_minus_exp_neg_ool(double x) { return 1.0 - exp(-x); }
-__device__ __forceinline__ double one_minus_exp_neg(double x) {
-    if (SPHRAY_COLD_OUTLINE) return one_minus_exp_neg_ool(x);
-    return 1.0 - exp(-x);
-}
-__device__ __forceinline__ double alpha_of(double x) {
-    if (SPHRAY_ALPHA_MODE == 1) {
-        if (x < 0.05) return x * (1.0 - x * (0.5 - x * (1.0 / 6.0 - x * (1.0 / 24.0))));
-        return 1.0 - static_cast<double>(__expf(-static_cast<float>(x)));
-    }
-    if (SPHRAY_ALPHA_MODE == 2) {  // series to x^4 below 2^-8, to x^6 below 1/16 (relative error < 7e-13)
-        if (x < 0x1p-8) {
-            double s = 1.0 / 120.0;
-            s = fma(s, -x, 1.0 / 24.0);
-            s = fma(s, -x, 1.0 / 6.0);
-            s = fma(s, -x, 0.5);
-            s = fma(s, -x, 1.0);
-            return s * x;
-        }
-        if (x < 0.0625) {
-            double s = 1.0 / 5040.0;
-            s = fma(s, -x, 1.0 / 720.0);
-            s = fma(s, -x, 1.0 / 120.0);
-            s = fma(s, -x, 1.0 / 24.0);
-            s = fma(s, -x, 1.0 / 6.0);
-            s = fma(s, -x, 0.5);
-            s = fma(s, -x, 1.0);
-            return s * x;
-        }
-        return one_minus_exp_neg(x);
-    }
+// alpha for x >= 2^-8: the series to x^6 below 1/16 (relative error < 7e-13),
+// else 1 - exp(-x) as the reference writes it (CUDA's exp is within 1 ulp of
+// glibc's; several hundred SASS instructions, hence out of line: at config 3
+// nearly every sample takes the short series).
+static __device__ __noinline__ double alpha_wide(double x) {
     if (x < 0.0625) {
-        double s = 1.0 / 40320.0;
-        s = fma(s, -x, 1.0 / 5040.0);
+        double s = 1.0 / 5040.0;
         s = fma(s, -x, 1.0 / 720.0);
         s = fma(s, -x, 1.0 / 120.0);
         s = fma(s, -x, 1.0 / 24.0);
@@ -208,7 +185,35 @@ __device__ __forceinline__ double alpha_of(double x) {
         s = fma(s, -x, 1.0);
         return s * x;
     }
-    return one_minus_exp_neg(x);
+    return 1.0 - exp(-x);
+}
+static __device__ __noinline__ double one_minus_exp_neg_ool(double x) { return 1.0 - exp(-x); }
+__device__ __forceinline__ double alpha_of(double x) {
+    if (SPHRAY_ALPHA_MODE == 1) {
+        if (x < 0.05) return x * (1.0 - x * (0.5 - x * (1.0 / 6.0 - x * (1.0 / 24.0))));
+        return 1.0 - static_cast<double>(__expf(-static_cast<float>(x)));
+    }
+    if (x < 0x1p-8) {  // series to x^4 (relative error < x^5/6! < 1.2e-15)
+        double s = 1.0 / 120.0;
+        s = fma(s, -x, 1.0 / 24.0);
+        s = fma(s, -x, 1.0 / 6.0);
+        s = fma(s, -x, 0.5);
+        s = fma(s, -x, 1.0);
+        return s * x;
+    }
+    if (SPHRAY_COLD_OUTLINE == 2) return alpha_wide(x);
+    if (x < 0.0625) {
+        double s = 1.0 / 5040.0;
+        s = fma(s, -x, 1.0 / 720.0);
+        s = fma(s, -x, 1.0 / 120.0);
+        s = fma(s, -x, 1.0 / 24.0);
+        s = fma(s, -x, 1.0 / 6.0);
+        s = fma(s, -x, 0.5);
+        s = fma(s, -x, 1.0);
+        return s * x;
+    }
+    if (SPHRAY_COLD_OUTLINE) return one_minus_exp_neg_ool(x);
+    return 1.0 - exp(-x);
 }
 
 // sphray_piece_mix (include/sphray_gpu.h) of one FieldPiece, for the per-ray
@@ -623,67 +628,57 @@ class RayWorker {
                          double& cg, double& cb, int& npc, int& nsmp) {
         if (k0 >= k1) return;
         int64_t tcur = pool_t(fs[k0]);
-        // One compositing site (the kernel is instruction-cache bound): the
-        // previous flush's open piece (lead lane) goes through the same call as
-        // the pieces of the run, in a virtual iteration before the first knot.
-        bool go = lead && comp;
-        int64_t cs = ot, ce = tcur;
+        if (lead && comp) cmp.composite_piece(ot, tcur, oa, stop, Tl, cr, cg, cb, nsmp);
         taylor_shift<D>(Pc, static_cast<uint64_t>(tcur) - static_cast<uint64_t>(tref));
         int64_t tn = tcur;
         // the last emitted piece's coefficients as doubles: the overflow test's
         // input for the next shift and the compositing input (one conversion)
         double A[D + 1];
 #pragma unroll
-        for (int d = 0; d <= D; ++d) A[d] = go ? to_double(oa[d]) : 0.0;
-        for (int k = go ? k0 - 1 : k0; k < k1; ++k) {
-            if (k >= k0) {
-                go = false;
-                const int s = fs[k];
-                const int64_t t = tn;
-                const bool more = k + 1 < nsel;
-                // the next knot's position and this knot's jumps are loaded
-                // before the shift: their shared-memory latency overlaps it
-                const int64_t tnext = more ? pool_t(fs[k + 1]) : t;
-                U jmp[D + 1];
+        for (int d = 0; d <= D; ++d) A[d] = 0.0;
+        for (int k = k0; k < k1; ++k) {
+            const int s = fs[k];
+            const int64_t t = tn;
+            const bool more = k + 1 < nsel;
+            // the next knot's position and this knot's jumps are loaded before
+            // the shift: their shared-memory latency overlaps it
+            const int64_t tnext = more ? pool_t(fs[k + 1]) : t;
+            U jmp[D + 1];
 #pragma unroll
-                for (int d = 1; d <= D; ++d) jmp[d] = pool_c(d, s);
-                if (t != tcur) {
-                    const uint64_t dl = static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur);
-                    taylor_shift<D>(Pc, dl);  // every shift follows an emission in this run
-                    if (SPHRAY_OVF_CHECK)
-                        aovf |= shift_overflows<D>(A, static_cast<double>(static_cast<int64_t>(dl)), Pc);
-                    tcur = t;
-                }
-#pragma unroll
-                for (int d = 1; d <= D; ++d) {
-                    Pc[d] = add_checked(Pc[d], jmp[d], aovf);
-                    if constexpr (DUMP && kW64) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
-                }
-                tn = tnext;
-                if (more && tn == t) continue;  // more jumps at this position
-                ++npc;
-#pragma unroll
-                for (int d = 0; d <= D; ++d) A[d] = to_double(Pc[d]);
-                if constexpr (DUMP && kW64)
-#pragma unroll
-                    for (int d = 0; d <= D; ++d) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
-                if constexpr (REC)
-                    if (P.ray_rec && !stop) csum += piece_mix<D, U>(t, Pc);
-                if constexpr (DUMP)
-                    if (!stop && P.dump_piece_t) dump_piece(t, Pc);
-                if (!more) {
-                    if (!stop) {
-                        open_p()[0] = static_cast<U>(static_cast<S>(t));
-#pragma unroll
-                        for (int d = 0; d <= D; ++d) open_p()[1 + d] = Pc[d];
-                    }
-                } else if (comp) {
-                    go = true;
-                    cs = t;
-                    ce = tn;
-                }
+            for (int d = 1; d <= D; ++d) jmp[d] = pool_c(d, s);
+            if (t != tcur) {
+                const uint64_t dl = static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur);
+                taylor_shift<D>(Pc, dl);  // every shift follows an emission in this run
+                if (SPHRAY_OVF_CHECK)
+                    aovf |= shift_overflows<D>(A, static_cast<double>(static_cast<int64_t>(dl)), Pc);
+                tcur = t;
             }
-            if (go) cmp.composite_piece_d(cs, ce, A, stop, Tl, cr, cg, cb, nsmp);
+#pragma unroll
+            for (int d = 1; d <= D; ++d) {
+                Pc[d] = add_checked(Pc[d], jmp[d], aovf);
+                if constexpr (DUMP && kW64) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
+            }
+            tn = tnext;
+            if (more && tn == t) continue;  // more jumps at this position
+            ++npc;
+#pragma unroll
+            for (int d = 0; d <= D; ++d) A[d] = to_double(Pc[d]);
+            if constexpr (DUMP && kW64)
+#pragma unroll
+                for (int d = 0; d <= D; ++d) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
+            if constexpr (REC)
+                if (P.ray_rec && !stop) csum += piece_mix<D, U>(t, Pc);
+            if constexpr (DUMP)
+                if (!stop && P.dump_piece_t) dump_piece(t, Pc);
+            if (!more) {
+                if (!stop) {
+                    open_p()[0] = static_cast<U>(static_cast<S>(t));
+#pragma unroll
+                    for (int d = 0; d <= D; ++d) open_p()[1 + d] = Pc[d];
+                }
+            } else if (comp) {
+                cmp.composite_piece_d(t, tn, A, stop, Tl, cr, cg, cb, nsmp);
+            }
         }
     }
 
