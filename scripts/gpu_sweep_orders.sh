@@ -1,7 +1,7 @@
 # config 4 order sweep: 4M blob, 1024^2, D in {1,2,3} x K in {1..4}
-mkdir -p gpurun_out
+mkdir -p gpurun_out; rm -f gpurun_out/sweep_summary.txt
 for D in 1 2 3; do for K in 1 2 3 4; do
-  timeout 600 python bench.py --config 4 --K $K --D $D --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 \
+  timeout 600 python bench.py --config 4 --K $K --D $D --steps 3 --warmup 3 --no-parity --exact-steps 0 --e2e-steps 0 \
     > gpurun_out/sweep_K${K}_D${D}.json 2> gpurun_out/sweep_K${K}_D${D}.err
   python -c "
 import json,sys; d=json.loads(open('gpurun_out/sweep_K${K}_D${D}.json').read().strip().splitlines()[-1])

@@ -435,3 +435,23 @@ def test_degree_one_small_tau_live_reference(ctx, K):
     assert np.abs(img.pixels - rgb).max() <= RGB_TOL
     for k in ("knots", "rays_touched", "int_ops", "residual_failures"):
         assert getattr(st, k) == rst[k], k
+
+
+def test_large_transfer_function_global_variant(ctx):
+    """A TF too large for the per-CTA shared copy (> 4 KB: 60 points) runs the
+    production kernel that reads it from global memory; same bars."""
+    v = np.linspace(-0.2, 2.5, 60)
+    tf = np.stack([v, 0.5 + 0.4 * np.sin(3 * v), 0.5 + 0.4 * np.cos(2 * v), 0.3 + 0.2 * np.sin(v),
+                   0.1 + 0.8 * v * v], axis=1)
+    ps, ck = _blob(5000, 48)
+    lut = S.load_lut(H.lut_path(4, 3, 1024))
+    rl = ref.Lut(H.lut_path(4, 3, 1024))
+    ds = S.dataset_stats(ps, lut)
+    qc = S.choose_quanta(lut, ds)
+    rds = ref.dataset_stats(ps, rl)
+    img, st = S.render_scene(ps, S.Camera(**ck), S.TransferFunction.from_array(tf), lut, qc, ds,
+                             S.RenderOptions(mode=S.MODE_EXACT), ctx=ctx)
+    rgb, rst, _, _ = ref.render_robust(ps, ref.Camera(**ck), tf, rl, ref.RpQuanta(qc.tau, qc.sigma, 64), rds)
+    assert np.abs(img.pixels - rgb).max() <= RGB_TOL
+    for k in ("knots", "rays_touched", "int_ops", "residual_failures"):
+        assert getattr(st, k) == rst[k], k
