@@ -167,6 +167,12 @@ __device__ __forceinline__ int sample_count(double len, double step, double inv_
 #ifndef SPHRAY_ALPHA_MODE
 #define SPHRAY_ALPHA_MODE 0  // 0: fp64 (series + exp); 1: round-1 fp32 (diagnostics)
 #endif
+#ifndef SPHRAY_PF_L1
+#define SPHRAY_PF_L1 1  // L1 prefetch of the candidate batch this many batches ahead (0: off)
+#endif
+#ifndef SPHRAY_SHIFT32
+#define SPHRAY_SHIFT32 1  // in-window Taylor shifts with a 32-bit delta
+#endif
 #ifndef SPHRAY_OVF_CHECK
 #define SPHRAY_OVF_CHECK 1  // genuine-overflow test of the merge (0: off, diagnostics only)
 #endif
@@ -584,6 +590,14 @@ class RayWorker {
         : P(p), w(wm), lane(l), tf_sa(t), cmp{p, t} {}
 
     __device__ __forceinline__ PT* pt_p() const { return static_cast<PT*>(w.pt); }
+    // Taylor shift by the distance between two positions of the window
+    // (below kSpan: 2^32 for the 32-bit offsets of int_width 32/64)
+    __device__ __forceinline__ static void win_shift(U (&v)[D + 1], uint64_t dl) {
+        if constexpr (kW64 && SPHRAY_SHIFT32)
+            taylor_shift<D>(v, static_cast<uint32_t>(dl));
+        else
+            taylor_shift<D>(v, dl);
+    }
     __device__ __forceinline__ int64_t pool_t(int slot) const {
         return tb + static_cast<int64_t>(pt_p()[slot]);
     }
@@ -648,7 +662,7 @@ class RayWorker {
             for (int d = 1; d <= D; ++d) jmp[d] = pool_c(d, s);
             if (t != tcur) {
                 const uint64_t dl = static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur);
-                taylor_shift<D>(Pc, dl);  // every shift follows an emission in this run
+                win_shift(Pc, dl);  // every shift follows an emission in this run
                 if (SPHRAY_OVF_CHECK)
                     aovf |= shift_overflows<D>(A, static_cast<double>(static_cast<int64_t>(dl)), Pc);
                 tcur = t;
@@ -710,19 +724,24 @@ class RayWorker {
             tref = pool_t(fs[0]);
             has_ref = true;
         }
+        // Sg = sum over the run of each knot's jumps shifted to tref, summed
+        // forward: the partial sum moves knot to knot by in-window (< 2^32)
+        // shifts and takes each knot's jumps (b_0 == 0 for every knot), and
+        // one shift carries it to tref -- modulo 2^64 the same value as
+        // shifting every knot to tref (shifts compose: p(y+a)(y+b) = p(y+a+b))
         U Sg[D + 1];
 #pragma unroll
         for (int d = 0; d <= D; ++d) Sg[d] = 0;
+        int64_t ta = k0 < k1 ? pool_t(fs[k0]) : tref;
         for (int k = k0; k < k1; ++k) {
             const int s = fs[k];
-            U g[D + 1];
-            g[0] = 0;  // b_0 == 0 for every knot
+            const int64_t t = pool_t(s);
+            if (t != ta) win_shift(Sg, static_cast<uint64_t>(t) - static_cast<uint64_t>(ta));
+            ta = t;
 #pragma unroll
-            for (int d = 1; d <= D; ++d) g[d] = pool_c(d, s);
-            taylor_shift<D>(g, static_cast<uint64_t>(tref) - static_cast<uint64_t>(pool_t(s)));
-#pragma unroll
-            for (int d = 0; d <= D; ++d) Sg[d] += g[d];
+            for (int d = 1; d <= D; ++d) Sg[d] += pool_c(d, s);
         }
+        taylor_shift<D>(Sg, static_cast<uint64_t>(tref) - static_cast<uint64_t>(ta));
         U E[D + 1];
 #pragma unroll
         for (int d = 0; d <= D; ++d) {
@@ -1132,6 +1151,13 @@ class RayWorker {
                     // consecutive records, both loads issued together)
                     mt = P.cmeta[c];
                     p = P.cxyzh[c];
+                    if (SPHRAY_PF_L1 && c + 32 * SPHRAY_PF_L1 < ce) {
+                        // pull a later batch's records from L2 into L1 while
+                        // this one is tested
+                        const uint32_t cn = c + 32 * SPHRAY_PF_L1;
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(P.cmeta + cn));
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(P.cxyzh + cn));
+                    }
                 }
                 if (c < ce) {
                     pi = mt.y;
