@@ -26,6 +26,12 @@ constexpr int kMaxJ = kMaxM * kMaxDegree;
 #ifndef SPHRAY_STAGE
 #define SPHRAY_STAGE 0
 #endif
+// SPHRAY_HQ_FRONT=1: the hit queue also keeps each hit's depth-sort front
+// (the flush bound of the first queued hit is then a shared-memory read, not
+// a dependent global load).
+#ifndef SPHRAY_HQ_FRONT
+#define SPHRAY_HQ_FRONT 1
+#endif
 
 #ifdef __CUDACC__
 #define SPHRAY_HD __host__ __device__
@@ -44,6 +50,9 @@ SPHRAY_HD inline size_t warp_bytes_for(int D, int cap, int jb = 8) {
     b += align16(static_cast<size_t>(jb) * (D + 2));  // open piece
     b += align16(sizeof(double) * kHitQueue * 2);     // hit queue: d2, t_chi
     b += align16(sizeof(int32_t) * kHitQueue);        // hit queue: particle
+#if SPHRAY_HQ_FRONT
+    b += align16(sizeof(float) * kHitQueue);          // hit queue: front
+#endif
     b += align16(sizeof(uint16_t) * cap * 2);         // ps, fl (+ flush set)
     b += align16(sizeof(uint32_t) * 256);             // radix bins
 #if SPHRAY_STAGE

@@ -320,6 +320,7 @@ struct WarpMem {
     double* hq_d2;  // hit queue (candidate order): squared distance of closest approach
     double* hq_t;
     int32_t* hq_p;
+    float* hq_f;    // SPHRAY_HQ_FRONT: the hit's particle front (depth-sort key)
     uint16_t* ps;   // pending slots, unsorted
     uint16_t* fl;   // free slot stack (+ the flush set above it)
     uint32_t* hist;  // 256: radix-sort bins
@@ -344,6 +345,8 @@ __device__ inline WarpMem carve(char* base, int D, int cap, int jb) {
     p += align16(sizeof(double) * kHitQueue * 2);
     w.hq_p = reinterpret_cast<int32_t*>(p);
     p += align16(sizeof(int32_t) * kHitQueue);
+    w.hq_f = reinterpret_cast<float*>(p);
+    if (SPHRAY_HQ_FRONT) p += align16(sizeof(float) * kHitQueue);
     w.ps = reinterpret_cast<uint16_t*>(p);
     w.fl = w.ps + cap;
     p += align16(sizeof(uint16_t) * cap * 2);
@@ -1068,6 +1071,11 @@ class RayWorker {
         return 0;
     }
 
+    // front (depth-sort key) of the first queued hit
+    __device__ __forceinline__ float head_front() const {
+        return SPHRAY_HQ_FRONT ? w.hq_f[0] : P.front[w.hq_p[0]];
+    }
+
     // Drop the first nq queued hits (up to 63 queued: shift in chunks of 32).
     __device__ __forceinline__ void drop_queued(int nq, int& hq_n) {
         const int rest = hq_n - nq;
@@ -1075,14 +1083,17 @@ class RayWorker {
             const int i = c0 + lane;
             int32_t qp = 0;
             double ql = 0.0, qt = 0.0;
+            float qf = 0.f;
             if (i < rest) {
                 qp = w.hq_p[nq + i];
+                if (SPHRAY_HQ_FRONT) qf = w.hq_f[nq + i];
                 ql = w.hq_d2[nq + i];
                 qt = w.hq_t[nq + i];
             }
             __syncwarp();
             if (i < rest) {
                 w.hq_p[i] = qp;
+                if (SPHRAY_HQ_FRONT) w.hq_f[i] = qf;
                 w.hq_d2[i] = ql;
                 w.hq_t[i] = qt;
             }
@@ -1170,6 +1181,7 @@ class RayWorker {
                 if (hit) {
                     const int at = hq_n + __popc(m & lanemask_lt());
                     w.hq_p[at] = static_cast<int32_t>(pi);
+                    if (SPHRAY_HQ_FRONT) w.hq_f[at] = __uint_as_float(mt.x);
                     w.hq_d2[at] = d2;
                     w.hq_t[at] = tchi;
                 }
@@ -1206,7 +1218,7 @@ class RayWorker {
                     stuck = round == 0;
                     break;
                 }
-                const int64_t F0 = knot_floor(P.front[w.hq_p[0]], P.inv_tau);
+                const int64_t F0 = knot_floor(head_front(), P.inv_tau);
                 const int rc = insert_hits(nq, F0);
                 if (rc == 1) return false;
                 if (rc == 2) {
@@ -1227,7 +1239,7 @@ class RayWorker {
             const bool final_ = hq_n == 0 && cursor >= ce;
             int64_t F = INT64_MAX;
             if (!final_) {
-                const float fr = hq_n > 0 ? P.front[w.hq_p[0]] : __uint_as_float(P.cmeta[cursor].x);
+                const float fr = hq_n > 0 ? head_front() : __uint_as_float(P.cmeta[cursor].x);
                 F = knot_floor(fr, P.inv_tau);
             }
             if (final_ || stuck || nfree < 32 * KN || np >= (P.cap * SPHRAY_FLUSH_AT) / 8) {
