@@ -892,11 +892,12 @@ void Engine::render(const sphray_camera& cam, const sphray_tf_point* tf, size_t 
     // is a heuristic; rays that still overflow go to the robust retry pass.)
     // int_width 32 frames run the robust variant too (its quantize and merge
     // carry the Checked<int32_t> range tests, render_kernel.cuh / quantize.cuh)
+    // (P.robust: 1 = rebasing only, 2 = with the int32 range tests.)
     const bool robust_frame = scene_extent_ / qc.tau > 2147483648.0 || w32 || w128;
-    P.robust = robust_frame ? 1 : 0;
+    P.robust = (w32 || w128) ? 2 : robust_frame ? 1 : 0;
     P.w128 = w128 ? 1 : 0;
     const size_t tfb =
-        (tfb_full <= 4096 && !dumps && !robust_frame && !std::getenv("SPHRAY_TF_GLOBAL")) ? tfb_full : 0;
+        (tfb_full <= 4096 && !dumps && !w32 && !w128 && !std::getenv("SPHRAY_TF_GLOBAL")) ? tfb_full : 0;
     P.tf_smem = static_cast<int>(tfb);
     auto best_shape = [&](int cap_, int& warps_, int& bps_) {
         const size_t wb_ = warp_smem_bytes(D, cap_, m, jb);

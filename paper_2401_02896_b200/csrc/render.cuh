@@ -103,7 +103,7 @@ struct FrameParams {
     int cap;         // knot slots per warp
     int warp_bytes;  // dynamic smem per warp
     int tf_smem;     // bytes of the per-CTA shared copy of tf after the windows (0: read global)
-    int robust;      // use the robust variant (rebasing window offsets) for this launch
+    int robust;      // robust variant for this launch: 1 = rebasing window offsets, 2 = + int32 range tests
     int w128;        // int_width 128: the robust variant with a modulo-2^128 merge
     // work distribution
     unsigned long long* work_counter;

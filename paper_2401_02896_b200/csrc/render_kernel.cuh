@@ -551,7 +551,7 @@ __device__ __noinline__ ReplayOut replay_run(const FrameParams& P, uint32_t tf_s
 // REC: the per-ray records (piece checksums) are compiled in; the production
 // kernel is instantiated with and without them (the checksum code costs ~2% of
 // the frame even when disabled at run time), the robust variant always has them.
-template <int D, int M, bool TS, bool DUMP, bool EVEN, bool REC, class U = uint64_t>
+template <int D, int M, bool TS, int DUMP, bool EVEN, bool REC, class U = uint64_t>
 class RayWorker {
    public:
     static constexpr int KN = 2 * M + 1;  // knots per hit, at most
@@ -567,6 +567,8 @@ class RayWorker {
     bool has_base = false;
     using S = SOf<U>;
     static constexpr bool kW64 = sizeof(U) == 8;
+    static constexpr bool kRobust = DUMP >= 1;  // rebasing + insert splitting
+    static constexpr bool kDump = DUMP >= 2;    // validation dumps + int32 range tests
     // window position offsets from tb: 32 bits (a live window spans < 2^32
     // quanta), 64 bits for int_width 128 (tiny tau: one particle's knots can
     // span more than 2^32 quanta)
@@ -673,19 +675,19 @@ class RayWorker {
 #pragma unroll
             for (int d = 1; d <= D; ++d) {
                 Pc[d] = add_checked(Pc[d], jmp[d], aovf);
-                if constexpr (DUMP && kW64) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
+                if constexpr (kDump && kW64) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
             }
             tn = tnext;
             if (more && tn == t) continue;  // more jumps at this position
             ++npc;
 #pragma unroll
             for (int d = 0; d <= D; ++d) A[d] = to_double(Pc[d]);
-            if constexpr (DUMP && kW64)
+            if constexpr (kDump && kW64)
 #pragma unroll
                 for (int d = 0; d <= D; ++d) narrow32(static_cast<int64_t>(Pc[d]), P.Q.w32, aovf);
             if constexpr (REC)
                 if (P.ray_rec && !stop) csum += piece_mix<D, U>(t, Pc);
-            if constexpr (DUMP)
+            if constexpr (kDump)
                 if (!stop && P.dump_piece_t) dump_piece(t, Pc);
             if (!more) {
                 if (!stop) {
@@ -936,12 +938,12 @@ class RayWorker {
         // F as an offset from tb, clamped to [0, kSpan]
         const uint64_t dF = static_cast<uint64_t>(F) - static_cast<uint64_t>(tb);
         const uint64_t Fo = all_ ? kSpan : (F <= tb ? 0ull : (dF > kSpan ? kSpan : dF));
-        // Robust variant (DUMP): every knot kept pending (and every later one)
+        // Robust variants (DUMP >= 1): every knot kept pending (and every later one)
         // is >= F, so the position base moves up to F in this pass and pt[]
         // offsets only span the live window, not the whole ray (small tau,
         // long rays).  The set being flushed keeps the old base until merged.
-        const int64_t tb_next = (DUMP && !all_ && F > tb) ? F : tb;
-        const PT keep_shift = (DUMP && Fo > 0 && Fo < kSpan) ? static_cast<PT>(Fo) : PT(0);
+        const int64_t tb_next = (kRobust && !all_ && F > tb) ? F : tb;
+        const PT keep_shift = (kRobust && Fo > 0 && Fo < kSpan) ? static_cast<PT>(Fo) : PT(0);
         PT tmin = ~PT(0), tmax = 0;
         PT* pt = pt_p();
         for (int c0 = 0; c0 < np; c0 += 32) {
@@ -1022,7 +1024,7 @@ class RayWorker {
         }
         bool ovf = false;
         HitPositions<M> hp;
-        bool emits = act && quantize_positions<M, EVEN, DUMP>(P.Q, h, lam, tchi, hp, ovf);
+        bool emits = act && quantize_positions<M, EVEN, kDump>(P.Q, h, lam, tchi, hp, ovf);
         int nk = emits ? hp.nk : 0;
         if (ovf) {
             report_overflow(pi);
@@ -1056,7 +1058,7 @@ class RayWorker {
                 for (int d = 1; d <= D; ++d) pool_c(d, slot) = static_cast<U>(b[d]);
                 w.ps[np + off + o] = static_cast<uint16_t>(slot);
             };
-            quantize_emit<D, M, EVEN, decltype(sink)&, DUMP, S>(P.Q, X, hp, ovf, sink);
+            quantize_emit<D, M, EVEN, decltype(sink)&, kDump, S>(P.Q, X, hp, ovf, sink);
             if (ovf) report_overflow(pi);
         }
         // a ray spanning more than 2^32 position quanta does not fit the
@@ -1185,7 +1187,7 @@ class RayWorker {
                     w.hq_d2[at] = d2;
                     w.hq_t[at] = tchi;
                 }
-                if (DUMP && P.dump_hit_ray && m) {
+                if (kDump && P.dump_hit_ray && m) {
                     unsigned long long base = 0;
                     if (lane == 0)
                         base = atomicAdd(&P.dump_count[0], static_cast<unsigned long long>(__popc(m)));
@@ -1226,7 +1228,7 @@ class RayWorker {
                     // main pass hands the ray to the robust retry variant,
                     // which finalises what it can (moving the base up to F0)
                     // and inserts fewer hits at a time
-                    if (!DUMP) return false;
+                    if (!kRobust) return false;
                     const int np0 = np;
                     flush(F0, false);
                     if (nq == 1 && np == np0) return false;  // no progress possible
@@ -1317,7 +1319,7 @@ class RayWorker {
 };
 
 // W128: the merge runs modulo 2^128 (int_width 128; robust variant only)
-template <int D, int M, bool TS, bool DUMP, bool EVEN, bool REC, bool W128 = false>
+template <int D, int M, bool TS, int DUMP, bool EVEN, bool REC, bool W128 = false>
 __global__ void __maxnreg__(SPHRAY_MAXNREG) k_render_rays(const __grid_constant__ FrameParams P) {
     using U = std::conditional_t<W128, unsigned __int128, uint64_t>;
     extern __shared__ __align__(16) char smem[];
@@ -1418,11 +1420,11 @@ __global__ void k_quantize_hits(const QuantParams Q, const sphray_particle* ps, 
 template <int D, int M, bool EVEN>
 int render_occupancy_tt(int warps, size_t smem) {
     int nb = 0;
-    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(rk::k_render_rays<D, M, true, false, EVEN, false>,
+    SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(rk::k_render_rays<D, M, true, 0, EVEN, false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
     SPHRAY_RK_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nb, rk::k_render_rays<D, M, true, false, EVEN, false>, warps * 32, smem));
+        &nb, rk::k_render_rays<D, M, true, 0, EVEN, false>, warps * 32, smem));
     return nb;
 }
 
@@ -1434,16 +1436,21 @@ int render_occupancy_t(int warps, size_t smem, bool even) {
 template <int D, int M, bool EVEN>
 void launch_render_tt(const FrameParams& P, int blocks, int warps, cudaStream_t s) {
     const size_t smem = static_cast<size_t>(P.warp_bytes) * warps + P.tf_smem;
-    // Validation dumps and the retry pass use the robust instantiation (dump
-    // code, per-flush rebasing of the 32-bit window offsets, batch splitting);
-    // the production kernel carries none of it (it is instruction-cache
-    // sensitive).  The robust variant reads the transfer function from global.
-    const bool robust = P.dump_hit_ray || P.dump_piece_t || P.ray_list || P.robust;
-    auto kern = P.w128 ? rk::k_render_rays<D, M, false, true, EVEN, true, true>
-                : robust ? rk::k_render_rays<D, M, false, true, EVEN, true>
-                : P.tf_smem ? (P.ray_rec ? rk::k_render_rays<D, M, true, false, EVEN, true>
-                                         : rk::k_render_rays<D, M, true, false, EVEN, false>)
-                            : rk::k_render_rays<D, M, false, false, EVEN, true>;
+    // Validation dumps, the retry pass and int_width 32 / 128 frames use the
+    // full robust instantiation (DUMP = 2: dump code, int32 range tests,
+    // per-flush rebasing of the 32-bit window offsets, batch splitting; TF in
+    // global memory).  Frames whose rays span more than 2^31 quanta (small
+    // tau) take the lean robust one (DUMP = 1: rebasing and splitting only,
+    // TF in shared memory).  The production kernel carries none of it (it is
+    // instruction-cache sensitive).
+    const bool full = P.dump_hit_ray || P.dump_piece_t || P.ray_list || P.robust == 2 ||
+                      (P.robust && !P.tf_smem);
+    auto kern = P.w128 ? rk::k_render_rays<D, M, false, 2, EVEN, true, true>
+                : full ? rk::k_render_rays<D, M, false, 2, EVEN, true>
+                : P.robust ? rk::k_render_rays<D, M, true, 1, EVEN, true>
+                : P.tf_smem ? (P.ray_rec ? rk::k_render_rays<D, M, true, 0, EVEN, true>
+                                         : rk::k_render_rays<D, M, true, 0, EVEN, false>)
+                            : rk::k_render_rays<D, M, false, 0, EVEN, true>;
     SPHRAY_RK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
     kern<<<blocks, warps * 32, smem, s>>>(P);
