@@ -66,7 +66,7 @@ def main():
     ap.add_argument("--rep")
     ap.add_argument("--launches")
     ap.add_argument("--cubin")
-    ap.add_argument("--kernel", default="k_render_raysILi3ELi2E")
+    ap.add_argument("--kernel", default="k_render_raysILi3ELi2ELb1ELb0ELb1ELb0ELb0E")
     ap.add_argument("--src", default=os.path.join(HERE, "..", "paper_2401_02896_b200", "csrc",
                                                  "render_kernel.cuh"))
     ap.add_argument("--title", default="render kernel profile")
@@ -136,11 +136,19 @@ def main():
                   "stalls_pct": {k: round(v / tot * 100, 2) for v, k in sorted(st, reverse=True)[:8]}}
             json.dump(ev, open(a.evidence, "w"), indent=1)
         if a.cubin:
+            cubin = a.cubin
+            if cubin.endswith(".o"):  # host object: pull the sm_100a cubin out of its fatbin
+                import glob
+                import tempfile
+                td = tempfile.mkdtemp()
+                subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(cubin)], cwd=td,
+                               capture_output=True)
+                cubin = sorted(glob.glob(os.path.join(td, "*.cubin")))[0]
             sass = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv",
                                    "--print-source", "sass"], capture_output=True, text=True).stdout
             tmp = a.out + ".sass.csv"
             open(tmp, "w").write(sass)
-            ph = subprocess.run([sys.executable, os.path.join(HERE, "phase_profile.py"), a.cubin,
+            ph = subprocess.run([sys.executable, os.path.join(HERE, "phase_profile.py"), cubin,
                                  a.kernel, tmp, a.src], capture_output=True, text=True).stdout
             os.remove(tmp)
             md += ["", "## Executed instructions by phase", "", "```", ph.strip(), "```"]
