@@ -66,7 +66,7 @@ def main():
     ap.add_argument("--rep")
     ap.add_argument("--launches")
     ap.add_argument("--cubin")
-    ap.add_argument("--kernel", default="k_render_raysILi3ELi2ELb1ELb0ELb1ELb0ELb0E")
+    ap.add_argument("--kernel", default="k_render_raysILi3ELi2ELb1ELi0ELb1ELb0ELb0E")
     ap.add_argument("--src", default=os.path.join(HERE, "..", "paper_2401_02896_b200", "csrc",
                                                  "render_kernel.cuh"))
     ap.add_argument("--title", default="render kernel profile")
