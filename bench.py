@@ -428,6 +428,14 @@ def run_ours(args):
             "note": "SURVEY.md 8(d): the path is instruction-issue bound once knots are never "
                     "materialised; the HBM fraction is tiny by construction.  traffic = ncu "
                     "dram__bytes of one render launch at this workload (profiles/)"}
+    # the bytes the chosen tiling streams, sum over tiles of
+    # |candidates(tile)| x (32 + 16 D), as the gather's HBM fraction
+    tb = st.candidates * comp_particle
+    roof["tiling"] = {"tile": "8x8 pixels", "candidates": st.candidates, "bytes": tb,
+                      "achieved": tb / (render_ms * 1e-3) / 1e9,
+                      "frac": tb / (render_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 7700.0),
+                      "formula": f"sum over tiles |candidates(tile)| * (32+16D) = "
+                                 f"{st.candidates} * {comp_particle}"}
     if ev:
         for k in ("issue_slots_busy_pct", "ipc", "warps_active_per_sm", "achieved_occupancy_pct",
                   "fp64_pipe_pct", "alu_pipe_pct", "fma_pipe_pct", "lsu_pipe_pct",
@@ -530,6 +538,11 @@ def run_ours(args):
                       "residual_failures": st.residual_failures,
                       "skipped_particles": st.skipped_particles,
                       "terminated_rays": st.terminated_rays},
+            # SURVEY.md 8(d)'s secondary rates of the timed (device-resident) frame
+            "rates": {"touched_rays_per_s": st.rays_touched / (render_ms * 1e-3),
+                      "hits_per_s": st.hits / (render_ms * 1e-3),
+                      "knots_per_s": st.knots / (render_ms * 1e-3),
+                      "int_ops_per_s": st.int_ops / (render_ms * 1e-3)},
             "setup_s": setup_s,
         }
         print(json.dumps(out), flush=True)
