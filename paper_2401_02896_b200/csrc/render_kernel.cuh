@@ -952,19 +952,22 @@ class RayWorker {
             const int s = valid ? w.ps[i] : 0;
             const PT t = valid ? pt[s] : PT(0);
             const bool sel = valid && static_cast<uint64_t>(t) < Fo;
+            // one ballot: the valid lanes are a prefix, so a kept lane's rank
+            // among the kept ones is (its lane) - (selected lanes below it)
             const unsigned msel = __ballot_sync(kFull, sel);
-            const unsigned mkeep = __ballot_sync(kFull, valid && !sel);
+            const int below = __popc(msel & lanemask_lt());
             __syncwarp();
             if (sel) {
-                fs[nsel + __popc(msel & lanemask_lt())] = static_cast<uint16_t>(s);
+                fs[nsel + below] = static_cast<uint16_t>(s);
                 tmin = t < tmin ? t : tmin;
                 tmax = t > tmax ? t : tmax;
             } else if (valid) {
-                w.ps[nkeep + __popc(mkeep & lanemask_lt())] = static_cast<uint16_t>(s);
+                w.ps[nkeep + lane - below] = static_cast<uint16_t>(s);
                 if (keep_shift) pt[s] = t - keep_shift;
             }
-            nsel += __popc(msel);
-            nkeep += __popc(mkeep);
+            const int ns = __popc(msel);
+            nsel += ns;
+            nkeep += min(32, np - c0) - ns;
         }
         __syncwarp();
         SPHRAY_KS(kStatFlushes, 1);
