@@ -665,13 +665,14 @@ class RayWorker {
             U jmp[D + 1];
 #pragma unroll
             for (int d = 1; d <= D; ++d) jmp[d] = pool_c(d, s);
-            if (t != tcur) {
-                const uint64_t dl = static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur);
-                win_shift(Pc, dl);  // every shift follows an emission in this run
-                if (SPHRAY_OVF_CHECK)
-                    aovf |= shift_overflows<D>(A, static_cast<double>(static_cast<int64_t>(dl)), Pc);
-                tcur = t;
-            }
+            // branch-free: a shift by 0 (more jumps at the position) is the
+            // identity; every nonzero shift follows an emission in this run,
+            // whose doubles A feed the overflow test
+            const uint64_t dl = static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur);
+            win_shift(Pc, dl);
+            if (SPHRAY_OVF_CHECK)
+                aovf |= (dl != 0) & shift_overflows<D>(A, static_cast<double>(static_cast<int64_t>(dl)), Pc);
+            tcur = t;
 #pragma unroll
             for (int d = 1; d <= D; ++d) {
                 Pc[d] = add_checked(Pc[d], jmp[d], aovf);
