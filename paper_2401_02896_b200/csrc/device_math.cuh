@@ -71,7 +71,8 @@ __device__ __forceinline__ bool hit_ray(const RayD& r, double cx, double cy, dou
 
 // hit_ray split in two for the render kernel: the predicate returns d2 and
 // t_chi; lam_of(d2, h) is the RayHit::lam of the same hit, computed later
-// (per queued hit, not per tested candidate).
+// (per queued hit, not per tested candidate).  No early exits: the gather
+// evaluates it on every lane and masks the result.
 __device__ __forceinline__ bool hit_test(const RayD& r, double cx, double cy, double cz,
                                          double support, double near_plane, double far_plane,
                                          double& d2_out, double& t_chi) {
@@ -79,11 +80,10 @@ __device__ __forceinline__ bool hit_test(const RayD& r, double cx, double cy, do
     const double t = dadd(dadd(dmul(ocx, r.dx), dmul(ocy, r.dy)), dmul(ocz, r.dz));
     const double d2 =
         dsub(dadd(dadd(dmul(ocx, ocx), dmul(ocy, ocy)), dmul(ocz, ocz)), dmul(t, t));
-    if (!(d2 < dmul(support, support))) return false;
-    if (dadd(t, support) <= near_plane || dsub(t, support) >= far_plane) return false;
     d2_out = d2;
     t_chi = t;
-    return true;
+    return (d2 < dmul(support, support)) & !(dadd(t, support) <= near_plane) &
+           !(dsub(t, support) >= far_plane);
 }
 __device__ __forceinline__ double lam_of(double d2, double h) {
     return ddiv(dsqrt(d2 < 0.0 ? 0.0 : d2), h);
