@@ -869,9 +869,12 @@ class RayWorker {
             reinterpret_cast<uint4*>(w.hist)[lane + 32] = make_uint4(0u, 0u, 0u, 0u);
             __syncwarp();
 #pragma unroll 1
-            for (int i = lane; i < nsel; i += 32) {
-                const uint32_t dg = static_cast<uint32_t>((pt[src[i]] - tmin) >> shift) & 255u;
-                atomicAdd(&w.hist[dg], 1u);
+            for (int c0 = 0; c0 < nsel; c0 += 32) {  // warp-uniform trip count
+                const int i = c0 + lane;
+                if (i < nsel) {
+                    const uint32_t dg = static_cast<uint32_t>((pt[src[i]] - tmin) >> shift) & 255u;
+                    atomicAdd(&w.hist[dg], 1u);
+                }
             }
             __syncwarp();
             // exclusive prefix of the 256 bins: 8 per lane
@@ -890,10 +893,13 @@ class RayWorker {
                 // the first pass needs no stability (the input order is
                 // arbitrary): atomic ranks
 #pragma unroll 1
-                for (int i = lane; i < nsel; i += 32) {
-                    const int sl = src[i];
-                    const uint32_t dg = static_cast<uint32_t>(pt[sl] - tmin) & 255u;
-                    dst[atomicAdd(&w.hist[dg], 1u)] = static_cast<uint16_t>(sl);
+                for (int c0 = 0; c0 < nsel; c0 += 32) {
+                    const int i = c0 + lane;
+                    if (i < nsel) {
+                        const int sl = src[i];
+                        const uint32_t dg = static_cast<uint32_t>(pt[sl] - tmin) & 255u;
+                        dst[atomicAdd(&w.hist[dg], 1u)] = static_cast<uint16_t>(sl);
+                    }
                 }
                 __syncwarp();
                 uint16_t* tmp = src;
