@@ -395,7 +395,7 @@ struct Compositor {
     // raycast.hpp:369-377): midpoints lo + (s + 1/2) dt as the reference
     // places them, taken here as the piece-local abscissa x = x0 + (s + 1/2) dx
     // (x0 = lo/tau - t_piece, dx = dt/tau; evaluate_piece, raycast.hpp:295-301)
-    // and fp64 Horner on sigma-scaled coefficients; alpha = 1 - exp(-ab dt)
+    // and fp64 Horner on the coefficients, times sigma; alpha = 1 - exp(-ab dt)
     // via alpha_of; colour and transmittance accumulate in fp64.  With `stop`
     // the reference's T > 1e-3 check runs before every sample (the
     // early-termination replay).  (Evaluating two samples per iteration for
@@ -406,6 +406,7 @@ struct Compositor {
         double acc = c[D];
 #pragma unroll
         for (int d = D - 1; d >= 0; --d) acc = fma(acc, x, c[d]);
+        acc *= P.Q.sigma;  // evaluate_piece (raycast.hpp:295-301): Horner on a_d, then x sigma
         double ab;
         if constexpr (TS)
             tf_sample(TfShared{tf_sa}, P.ntf, acc, r, g, b, ab);
@@ -434,8 +435,8 @@ struct Compositor {
 
     // Per-piece setup of composite() (raycast.hpp:364-372): [lo, hi] =
     // [t_s tau, t_e tau] cut to [near, far], n = max(2, ceil((hi-lo)/step))
-    // samples of width dt = (hi-lo)/n, the piece polynomial in double scaled
-    // by sigma, and the piece-local abscissa x0 + (s + 1/2) dx of sample s.
+    // samples of width dt = (hi-lo)/n, the piece polynomial in double, and
+    // the piece-local abscissa x0 + (s + 1/2) dx of sample s.
     // Returns 0 when nothing is sampled (empty interval, or a zero piece
     // under a transfer function that is clear at 0: alpha = 1 - exp(-0) = 0).
     template <class U>
@@ -464,7 +465,7 @@ struct Compositor {
 #pragma unroll
         for (int d = 0; d <= D; ++d) {
             zero &= A[d] == 0.0;
-            c[d] = A[d] * P.Q.sigma;
+            c[d] = A[d];
         }
         if (zero && P.tf0_clear) return 0;
         x0 = fma(lo, P.inv_tau, -static_cast<double>(ts));
