@@ -421,10 +421,12 @@ struct Compositor {
                                                  double& cb) const {
         Tout = T0;
         cr = cg = cb = 0.0;
+        double sh = 0.5;  // s + 1/2 carried as a double (exact; no int -> double per sample)
         for (int s = 0; s < n; ++s) {
             if (stop && !(Tout > 1e-3)) break;
             double a, r, g, b;
-            sample_eval(c, fma(static_cast<double>(s) + 0.5, dx, x0), dt, a, r, g, b);
+            sample_eval(c, fma(sh, dx, x0), dt, a, r, g, b);
+            sh += 1.0;
             const double ta = Tout * a;
             cr = fma(ta, r, cr);
             cg = fma(ta, g, cg);
