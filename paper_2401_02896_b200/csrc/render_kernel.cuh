@@ -341,12 +341,12 @@ __device__ inline WarpMem carve(char* base, int D, int cap, int jb) {
     w.open = p;
     p += align16(static_cast<size_t>(jb) * (D + 2));
     w.hq_d2 = reinterpret_cast<double*>(p);
-    w.hq_t = w.hq_d2 + kHitQueue;
-    p += align16(sizeof(double) * kHitQueue * 2);
+    w.hq_t = w.hq_d2 + kHqSlots;
+    p += align16(sizeof(double) * kHqSlots * 2);
     w.hq_p = reinterpret_cast<int32_t*>(p);
-    p += align16(sizeof(int32_t) * kHitQueue);
+    p += align16(sizeof(int32_t) * kHqSlots);
     w.hq_f = reinterpret_cast<float*>(p);
-    if (SPHRAY_HQ_FRONT) p += align16(sizeof(float) * kHitQueue);
+    if (SPHRAY_HQ_FRONT) p += align16(sizeof(float) * kHqSlots);
     w.ps = reinterpret_cast<uint16_t*>(p);
     w.fl = w.ps + cap;
     p += align16(sizeof(uint16_t) * cap * 2);
@@ -1197,8 +1197,9 @@ class RayWorker {
                                          far_plane, d2, tchi);
                 }
                 const unsigned m = __ballot_sync(kFull, hit);
-                if (hit) {
-                    const int at = hq_n + __popc(m & lanemask_lt());
+                {
+                    // no branch: lanes without a hit store to the dummy slot
+                    const int at = hit ? hq_n + __popc(m & lanemask_lt()) : kHitQueue;
                     w.hq_p[at] = static_cast<int32_t>(pi);
                     if (SPHRAY_HQ_FRONT) w.hq_f[at] = __uint_as_float(mt.x);
                     w.hq_d2[at] = d2;
