@@ -286,7 +286,10 @@ __device__ __forceinline__ uint64_t piece_mix(int64_t t, const U (&a)[D + 1]) {
 // left int64 -- the case where render_scene<int64_t> throws OverflowError and
 // a wrapped merge would silently give a wrong field.  A non-finite prediction
 // (astronomic terms) counts as overflow too.
-template <int D, class U>
+// TOP = false skips order D: a Taylor shift leaves the top coefficient
+// unchanged, so when v is the exact double image of the shifted state's own
+// pre-shift integers (the walk), that order cannot differ.
+template <int D, class U, bool TOP = true>
 __device__ __forceinline__ bool shift_overflows(const double (&v)[D + 1], double delta,
                                                 const U (&w)[D + 1]) {
     constexpr double kLim = sizeof(U) == 16 ? 0x1p126 : 0x1p62;
@@ -300,7 +303,7 @@ __device__ __forceinline__ bool shift_overflows(const double (&v)[D + 1], double
         for (int j = D - 1; j >= i; --j) p[j] = fma(delta, p[j + 1], p[j]);
     bool bad = false;
 #pragma unroll
-    for (int d = 0; d <= D; ++d)
+    for (int d = 0; d <= (TOP ? D : D - 1); ++d)
         bad |= !(fabs(p[d] - to_double(w[d])) < kLim);
     return bad;
 }
@@ -674,7 +677,7 @@ class RayWorker {
             const uint64_t dl = static_cast<uint64_t>(t) - static_cast<uint64_t>(tcur);
             win_shift(Pc, dl);
             if (SPHRAY_OVF_CHECK)
-                aovf |= (dl != 0) & shift_overflows<D>(A, static_cast<double>(static_cast<int64_t>(dl)), Pc);
+                aovf |= (dl != 0) & shift_overflows<D, U, false>(A, static_cast<double>(static_cast<int64_t>(dl)), Pc);
             tcur = t;
 #pragma unroll
             for (int d = 1; d <= D; ++d) {
